@@ -1,0 +1,145 @@
+"""CPU oracle for DIP candidate-schedule scoring -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package. It shares no code with the CUDA path
+(paper_2504_14145_b200/) and never imports it; both read the same seeded
+inputs from gen/ (data only).
+
+The arithmetic lives in oracle/dip_oracle.c (plain C, O1-O11 of SURVEY.md
+§8(c), each step citing the PAPER.md passage it follows). This wrapper only
+marshals numpy arrays. Every function is pinned by tests/test_oracle_*.py
+(see DESIGN.md §4 for the pin of each step).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dip_oracle.c")
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+ST_OK, ST_OOM, ST_DEADLOCK, ST_BAD = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain -O2 (no SIMD tricks: it is the slow reference)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", _SO, _SRC])
+    return _SO
+
+
+class _OProblem(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_uint32), ("nmod", ctypes.c_uint32), ("m", ctypes.c_uint32)] + \
+        [(k, ctypes.c_void_p) for k in ("L", "K", "max_split", "w_max", "producer_mask", "tab_off",
+                                        "tab_f", "tab_b", "tab_act", "tab_p2p", "chunk_off",
+                                        "chunk_layers", "inst_off", "inst_units", "budget_kib")]
+
+
+class _OCands(ctypes.Structure):
+    _fields_ = [("n_max", ctypes.c_uint32), ("fbw", ctypes.c_uint32)] + \
+        [(k, ctypes.c_void_p) for k in ("split", "n", "fwd", "bwd", "fb")]
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        lib.oracle_chunk_layers.restype = ctypes.c_int
+        lib.oracle_chunk_layers.argtypes = [ctypes.c_uint32] * 3 + [ctypes.c_void_p]
+        lib.oracle_split.restype = ctypes.c_int
+        lib.oracle_split.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
+        lib.oracle_eval.restype = ctypes.c_int
+        lib.oracle_eval.argtypes = [ctypes.POINTER(_OProblem), ctypes.POINTER(_OCands), ctypes.c_uint64,
+                                    ctypes.c_uint64] + [ctypes.c_void_p] * 6 + [ctypes.c_int]
+        lib.oracle_timeline.restype = ctypes.c_int
+        lib.oracle_timeline.argtypes = [ctypes.POINTER(_OProblem), ctypes.POINTER(_OCands), ctypes.c_uint64,
+                                        ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_argmin.restype = ctypes.c_int64
+        lib.oracle_argmin.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
+        _lib = lib
+    return _lib
+
+
+def chunk_layers(L: int, P: int, K: int):
+    """O1 (R-3): layers per chunk, or None if P*K > L (TooManyChunks)."""
+    out = np.zeros(max(1, P * K), np.uint32)
+    rc = _load().oracle_chunk_layers(L, P, K, out.ctypes.data)
+    return None if rc != 0 else [int(v) for v in out[:P * K]]
+
+
+def split_sizes(N: int, M: int):
+    """O2 (R-2): sizes of the M balanced contiguous parts of N instances."""
+    st = np.zeros(M + 1, np.uint32)
+    _load().oracle_split(N, M, st.ctypes.data)
+    return [int(st[j + 1] - st[j]) for j in range(M)]
+
+
+class _Bound:
+    """Keeps the numpy arrays alive while C holds pointers into them."""
+
+    def __init__(self, pb, cands):
+        from gen.problem import problem_arrays
+        a = problem_arrays(pb)
+        self.keep = dict(a)
+        self.keep["inst_off"] = np.ascontiguousarray(pb.inst_off, np.uint32)
+        self.keep["inst_units"] = np.ascontiguousarray(pb.inst_units, np.uint16)
+        self.keep["budget_kib"] = np.ascontiguousarray(pb.budget_kib, np.uint32)
+        k = self.keep
+        self.pb = _OProblem(pb.P, pb.nmod, pb.m, *[k[n].ctypes.data for n in (
+            "L", "K", "max_split", "w_max", "producer_mask", "tab_off", "tab_f", "tab_b", "tab_act", "tab_p2p",
+            "chunk_off", "chunk_layers", "inst_off", "inst_units", "budget_kib")])
+        self.c = cands
+        self.cs = _OCands(pb.n_max, pb.fbw, *[np.ascontiguousarray(getattr(cands, n)).ctypes.data
+                                              for n in ("split", "n", "fwd", "bwd", "fb")])
+
+
+class Results:
+    def __init__(self, count: int, P: int):
+        self.makespan = np.zeros(count, np.uint64)
+        self.status = np.zeros(count, np.uint32)
+        self.oom_mask = np.zeros(count, np.uint32)
+        self.bubble = np.zeros(count, np.float64)
+        self.peaks = np.zeros((count, P), np.uint64)
+        self.busy = np.zeros(count, np.uint64)
+
+
+def evaluate(pb, cands, first: int = 0, count: Optional[int] = None, threads: int = 1) -> Results:
+    """O1-O10 for candidates [first, first+count) of the host-view batch `cands`."""
+    for n in ("split", "n", "fwd", "bwd", "fb"):
+        assert getattr(cands, n).flags["C_CONTIGUOUS"], n
+    if count is None:
+        count = cands.count - first
+    lib = _load()
+    bd = _Bound(pb, cands)
+    res = Results(count, pb.P)
+    lib.oracle_eval(ctypes.byref(bd.pb), ctypes.byref(bd.cs), first, count, res.makespan.ctypes.data,
+                    res.status.ctypes.data, res.oom_mask.ctypes.data, res.bubble.ctypes.data,
+                    res.peaks.ctypes.data, res.busy.ctypes.data, threads)
+    return res
+
+
+def timeline(pb, cands, x: int):
+    """Per-(rank, slot) (start, end) arrays of candidate x, shape [P, 2n]; None unless timed."""
+    lib = _load()
+    bd = _Bound(pb, cands)
+    n = int(cands.n[x])
+    st = np.zeros(max(1, pb.P * 2 * n), np.uint64)
+    en = np.zeros_like(st)
+    status = lib.oracle_timeline(ctypes.byref(bd.pb), ctypes.byref(bd.cs), x, st.ctypes.data, en.ctypes.data)
+    if status not in (ST_OK, ST_OOM):
+        return status, None, None
+    return status, st[:pb.P * 2 * n].reshape(pb.P, 2 * n), en[:pb.P * 2 * n].reshape(pb.P, 2 * n)
+
+
+def argmin(makespan: np.ndarray, status: np.ndarray) -> int:
+    """O11 (R-14, R-15): lowest index among the OK candidates of minimal makespan."""
+    ms = np.ascontiguousarray(makespan, np.uint64)
+    st = np.ascontiguousarray(status, np.uint32)
+    return int(_load().oracle_argmin(ms.ctypes.data, st.ctypes.data, len(ms)))

@@ -1,0 +1,366 @@
+/* dip_oracle.c -- the CPU ORACLE for DIP candidate-schedule scoring.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this file's
+ * library.  It shares no code, header, table or helper with the CUDA path
+ * (paper_2504_14145_b200/), and never imports it.
+ *
+ * A plain, slow, obviously-correct simulator of one candidate schedule, written
+ * step by step in the order of SURVEY.md §8(c) (O1-O11) and of the paper:
+ *
+ *   O1  chunking           P:457-459 "distributes layers across P*K_i model chunks" (R-3)
+ *   O2  split              P:461-467 "M_i ... uniformly partitioned sub-microbatches" (R-2, R-21)
+ *   O3  segments           P:466-467 "2 M_i K_i pipeline segments"
+ *   O4  encoding checks    (R-11)
+ *   O5  per-rank orders    (R-1)
+ *   O6  stage costs        P:522-523 (simulator latencies), P:685-700 (R-7, R-20)
+ *   O7  explicit edge list P:368 (segments span all P ranks), R-4..R-6
+ *   O8  Kahn longest path  P:702 "populates operator timestamps in topological order" (R-12)
+ *   O9  memory timeline    P:703-705 "tensor lifetimes ... peak memory usage" (R-9, R-10)
+ *   O10 outputs            P:499 score = "end-to-end iteration time"; bubble P:248 (R-16)
+ *   O11 argmin             P:499-501 best score; ties -> lowest index (R-14, R-15)
+ *
+ * Integers everywhere (ns, KiB); u64 accumulators.  The only floating-point
+ * value, the bubble ratio, is one IEEE double division of two exact integers.
+ * Multi-threaded only across candidates (pthreads).
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+    uint32_t P, nmod, m;
+    const uint32_t *L, *K, *max_split, *w_max, *producer_mask;   /* [nmod] */
+    const uint32_t *tab_off;                                      /* [nmod+1] */
+    const uint32_t *tab_f, *tab_b, *tab_act, *tab_p2p;            /* per-layer T_i[W] */
+    const uint32_t *chunk_off;      /* [nmod+1]; empty range -> default O1 rule */
+    const uint32_t *chunk_layers;   /* explicit layers per chunk (P*K_i entries) */
+    const uint32_t *inst_off;       /* [m*nmod+1] */
+    const uint16_t *inst_units;
+    const uint32_t *budget_kib;     /* [P] */
+} oproblem;
+
+typedef struct {
+    uint32_t n_max, fbw;
+    const uint8_t *split;           /* [N][m*nmod] */
+    const uint32_t *n;              /* [N] */
+    const uint16_t *fwd, *bwd;      /* [N][n_max] */
+    const uint32_t *fb;             /* [N][P][fbw] */
+} ocands;
+
+enum { ST_OK = 0, ST_OOM = 1, ST_DEADLOCK = 2, ST_BAD = 3 };
+
+/* ---------------- O1: layers per chunk (R-3) ----------------
+ * C = P*K chunks of consecutive layers; the first L mod C chunks get one extra
+ * layer.  Segment k on rank r uses chunk k*P + r.  C > L is an error. */
+int oracle_chunk_layers(uint32_t L, uint32_t P, uint32_t K, uint32_t *out) {
+    uint32_t C = P * K;
+    if (C == 0 || C > L) return -1;
+    for (uint32_t c = 0; c < C; c++) out[c] = L / C + (c < L % C ? 1u : 0u);
+    return 0;
+}
+
+/* ---------------- O2: balanced contiguous split (R-2) ----------------
+ * Part j of N instances split M ways covers [j*q + min(j, rho), (j+1)*q + min(j+1, rho))
+ * with q = floor(N/M), rho = N mod M.  start has M+1 entries. */
+int oracle_split(uint32_t N, uint32_t M, uint32_t *start) {
+    if (M == 0) return -1;
+    uint32_t q = N / M, rho = N % M;
+    for (uint32_t j = 0; j <= M; j++) start[j] = j * q + (j < rho ? j : rho);
+    return 0;
+}
+
+typedef struct {
+    uint64_t makespan, busy;
+    uint32_t status, oom_mask;
+    double bubble;
+} ores;
+
+static uint32_t seg_count_max(const oproblem *pb) {
+    uint32_t t = 0;
+    for (uint32_t i = 0; i < pb->nmod; i++) t += pb->max_split[i] * pb->K[i];
+    return t * pb->m;
+}
+
+/* layers of module i, chunk c (O1, or the explicit override) */
+static uint32_t layers_of(const oproblem *pb, uint32_t i, uint32_t c) {
+    uint32_t lo = pb->chunk_off[i], hi = pb->chunk_off[i + 1];
+    if (hi > lo) return pb->chunk_layers[lo + c];
+    uint32_t C = pb->P * pb->K[i], L = pb->L[i];
+    return L / C + (c < L % C ? 1u : 0u);
+}
+
+/* Evaluate candidate x.  peaks: [P] (u64), may be NULL.  If tl_start/tl_end are
+ * given they receive per (rank, slot) start/end times ([P][2n]). */
+static void eval_one(const oproblem *pb, const ocands *cs, uint64_t x, ores *res, uint64_t *peaks,
+                     uint64_t *tl_start, uint64_t *tl_end) {
+    const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
+    const uint32_t n_max = cs->n_max, fbw = cs->fbw;
+    const uint8_t *split = cs->split + x * (uint64_t)m * nm;
+    const uint16_t *fwd = cs->fwd + x * (uint64_t)n_max;
+    const uint16_t *bwd = cs->bwd + x * (uint64_t)n_max;
+    const uint32_t *fb = cs->fb + x * (uint64_t)P * fbw;
+    uint32_t ncand = cs->n[x];
+
+    res->makespan = UINT64_MAX;
+    res->busy = 0;
+    res->status = ST_BAD;
+    res->oom_mask = 0;
+    res->bubble = -1.0;
+    if (peaks) for (uint32_t r = 0; r < P; r++) peaks[r] = 0;
+
+    /* segment-id space: id(b,i,j,k) = base(b,i) + j*K_i + k, b-major */
+    uint32_t idmax = seg_count_max(pb);
+    uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
+    uint32_t *W = calloc(idmax + 1, sizeof(uint32_t));       /* work units of the segment's part */
+    uint8_t *present = calloc(idmax + 1, 1);
+    uint32_t *sb = malloc(sizeof(uint32_t) * (idmax + 1)), *si = malloc(sizeof(uint32_t) * (idmax + 1));
+    uint32_t *sj = malloc(sizeof(uint32_t) * (idmax + 1)), *sk = malloc(sizeof(uint32_t) * (idmax + 1));
+    int bad = 0;
+    uint32_t acc = 0, n = 0;
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            base[b * nm + i] = acc;
+            for (uint32_t j = 0; j < pb->max_split[i]; j++)
+                for (uint32_t k = 0; k < pb->K[i]; k++) {
+                    uint32_t id = acc + j * pb->K[i] + k;
+                    sb[id] = b; si[id] = i; sj[id] = j; sk[id] = k;
+                }
+            acc += pb->max_split[i] * pb->K[i];
+        }
+    /* O2: split and work per part */
+    for (uint32_t b = 0; b < m && !bad; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            uint32_t q = b * nm + i;
+            uint32_t lo = pb->inst_off[q], N = pb->inst_off[q + 1] - lo, M = split[q];
+            uint32_t cap = N < pb->max_split[i] ? N : pb->max_split[i];
+            if ((N == 0) != (M == 0) || M > cap) { bad = 1; break; }
+            if (M == 0) continue;
+            uint32_t st[16];
+            oracle_split(N, M, st);
+            for (uint32_t j = 0; j < M; j++) {
+                uint32_t w = 0;
+                for (uint32_t u = st[j]; u < st[j + 1]; u++) w += pb->inst_units[lo + u];
+                for (uint32_t k = 0; k < pb->K[i]; k++) {
+                    uint32_t id = base[q] + j * pb->K[i] + k;
+                    present[id] = 1;
+                    W[id] = w;
+                    n++;   /* O3 */
+                }
+            }
+        }
+    /* O4: encoding checks */
+    if (!bad && (ncand != n || n > n_max)) bad = 1;
+    if (!bad) {
+        uint8_t *seenF = calloc(idmax + 1, 1), *seenB = calloc(idmax + 1, 1);
+        for (uint32_t p = 0; p < n_max && !bad; p++) {
+            if (p < n) {
+                uint32_t a = fwd[p], c = bwd[p];
+                if (a >= idmax || c >= idmax || !present[a] || !present[c] || seenF[a] || seenB[c]) bad = 1;
+                else { seenF[a] = 1; seenB[c] = 1; }
+            } else if (fwd[p] != 0xFFFF || bwd[p] != 0xFFFF) bad = 1;
+        }
+        free(seenF); free(seenB);
+        for (uint32_t r = 0; r < P && !bad; r++) {
+            uint32_t ones = 0;
+            for (uint32_t t = 0; t < 32 * fbw; t++) {
+                uint32_t bit = (fb[r * fbw + t / 32] >> (t % 32)) & 1u;
+                if (t < 2 * n) ones += bit;
+                else if (bit) bad = 1;
+            }
+            if (ones != n) bad = 1;
+        }
+    }
+    if (bad) goto done;
+    if (n == 0) {
+        res->makespan = 0;
+        res->status = ST_OK;
+        res->bubble = 0.0;
+        goto done;
+    }
+    {
+        const uint32_t S = 2 * n, NN = P * S;
+        /* O5: per-rank orders; O6: costs */
+        uint8_t *dir = malloc(NN);
+        uint32_t *seg = malloc(sizeof(uint32_t) * NN);
+        uint64_t *lat = malloc(sizeof(uint64_t) * NN), *act = malloc(sizeof(uint64_t) * NN);
+        uint32_t *slotF = malloc(sizeof(uint32_t) * P * (idmax + 1)), *slotB = malloc(sizeof(uint32_t) * P * (idmax + 1));
+        for (uint32_t r = 0; r < P; r++) {
+            uint32_t fi = 0, bi = 0;
+            for (uint32_t t = 0; t < S; t++) {
+                uint32_t node = r * S + t, isb = (fb[r * fbw + t / 32] >> (t % 32)) & 1u, s;
+                if (isb) { s = bwd[bi++]; slotB[r * (idmax + 1) + s] = t; }
+                else { s = fwd[fi++]; slotF[r * (idmax + 1) + s] = t; }
+                dir[node] = (uint8_t)isb;
+                seg[node] = s;
+                uint32_t i = si[s], k = sk[s];
+                uint32_t toff = pb->tab_off[i] + W[s];
+                uint64_t lay = layers_of(pb, i, k * P + r);
+                lat[node] = lay * (uint64_t)(isb ? pb->tab_b[toff] : pb->tab_f[toff]);
+                act[node] = lay * (uint64_t)pb->tab_act[toff];
+            }
+        }
+        /* O7: explicit predecessor lists (dst node, src node, weight) */
+        uint32_t cap = NN * 4 + 16, ne = 0;
+        uint32_t *esrc = malloc(sizeof(uint32_t) * cap), *edst = malloc(sizeof(uint32_t) * cap);
+        uint64_t *ew = malloc(sizeof(uint64_t) * cap);
+#define ADD_EDGE(SRC, DST, WT) do { \
+        if (ne == cap) { cap *= 2; esrc = realloc(esrc, sizeof(uint32_t) * cap); \
+            edst = realloc(edst, sizeof(uint32_t) * cap); ew = realloc(ew, sizeof(uint64_t) * cap); } \
+        esrc[ne] = (SRC); edst[ne] = (DST); ew[ne] = (WT); ne++; } while (0)
+        for (uint32_t r = 0; r < P; r++)
+            for (uint32_t t = 0; t < S; t++) {
+                uint32_t node = r * S + t, s = seg[node];
+                uint32_t b = sb[s], i = si[s], k = sk[s], K = pb->K[i];
+                uint64_t p2p_s = pb->tab_p2p[pb->tab_off[i] + W[s]];
+                if (t > 0) ADD_EDGE(node - 1, node, 0);                 /* same rank, previous slot */
+                if (dir[node] == 0) {                                    /* forward stage */
+                    if (r > 0) ADD_EDGE((r - 1) * S + slotF[(r - 1) * (idmax + 1) + s], node, p2p_s); /* R-4 */
+                    else if (k > 0) {                                    /* previous segment, rank P-1 */
+                        uint32_t pr = s - 1;
+                        uint64_t wgt = P > 1 ? pb->tab_p2p[pb->tab_off[i] + W[pr]] : 0;
+                        ADD_EDGE((P - 1) * S + slotF[(P - 1) * (idmax + 1) + pr], node, wgt);
+                    } else {                                             /* producer join (R-5) */
+                        for (uint32_t ip = 0; ip < nm; ip++) {
+                            if (!((pb->producer_mask[i] >> ip) & 1u)) continue;
+                            for (uint32_t jp = 0; jp < split[b * nm + ip]; jp++) {
+                                uint32_t pr = base[b * nm + ip] + jp * pb->K[ip] + pb->K[ip] - 1;
+                                uint64_t wgt = P > 1 ? pb->tab_p2p[pb->tab_off[ip] + W[pr]] : 0;
+                                ADD_EDGE((P - 1) * S + slotF[(P - 1) * (idmax + 1) + pr], node, wgt);
+                            }
+                        }
+                    }
+                } else {                                                 /* backward stage */
+                    if (r + 1 < P) ADD_EDGE((r + 1) * S + slotB[(r + 1) * (idmax + 1) + s], node, p2p_s);
+                    else if (k + 1 < K) {                                /* next segment, rank 0 */
+                        ADD_EDGE(0 * S + slotB[0 * (idmax + 1) + s + 1], node, P > 1 ? p2p_s : 0);
+                    } else {
+                        int any = 0;                                     /* consumer join (R-5) */
+                        for (uint32_t ic = 0; ic < nm; ic++) {
+                            if (!((pb->producer_mask[ic] >> i) & 1u)) continue;
+                            for (uint32_t jc = 0; jc < split[b * nm + ic]; jc++) {
+                                uint32_t cn = base[b * nm + ic] + jc * pb->K[ic];
+                                ADD_EDGE(0 * S + slotB[0 * (idmax + 1) + cn], node, P > 1 ? p2p_s : 0);
+                                any = 1;
+                            }
+                        }
+                        if (!any)                                        /* loss turnaround (R-6) */
+                            ADD_EDGE((P - 1) * S + slotF[(P - 1) * (idmax + 1) + s], node, 0);
+                    }
+                }
+            }
+#undef ADD_EDGE
+        /* O8: Kahn with a FIFO queue */
+        uint32_t *indeg = calloc(NN, sizeof(uint32_t)), *soff = calloc(NN + 1, sizeof(uint32_t));
+        for (uint32_t e = 0; e < ne; e++) { indeg[edst[e]]++; soff[esrc[e] + 1]++; }
+        for (uint32_t v = 0; v < NN; v++) soff[v + 1] += soff[v];
+        uint32_t *sorder = malloc(sizeof(uint32_t) * (ne + 1)), *fill = calloc(NN, sizeof(uint32_t));
+        for (uint32_t e = 0; e < ne; e++) sorder[soff[esrc[e]] + fill[esrc[e]]++] = e;
+        uint64_t *start = calloc(NN, sizeof(uint64_t)), *end = calloc(NN, sizeof(uint64_t));
+        uint32_t *queue = malloc(sizeof(uint32_t) * NN), qh = 0, qt = 0;
+        for (uint32_t v = 0; v < NN; v++) if (indeg[v] == 0) queue[qt++] = v;
+        while (qh < qt) {
+            uint32_t v = queue[qh++];
+            end[v] = start[v] + lat[v];
+            for (uint32_t q = soff[v]; q < soff[v + 1]; q++) {
+                uint32_t e = sorder[q], d = edst[e];
+                uint64_t cand = end[v] + ew[e];
+                if (cand > start[d]) start[d] = cand;
+                if (--indeg[d] == 0) queue[qt++] = d;
+            }
+        }
+        /* O9: memory per rank in slot order (order only; also for DEADLOCK) */
+        uint32_t oom = 0;
+        for (uint32_t r = 0; r < P; r++) {
+            uint64_t cur = 0, peak = 0;
+            for (uint32_t t = 0; t < S; t++) {
+                uint32_t node = r * S + t;
+                if (dir[node] == 0) { cur += act[node]; if (cur > peak) peak = cur; }
+                else cur -= act[node];
+            }
+            if (peaks) peaks[r] = peak;
+            if (peak > pb->budget_kib[r]) oom |= 1u << r;
+        }
+        res->oom_mask = oom;
+        if (qt < NN) {
+            res->status = ST_DEADLOCK;            /* fewer than P*2n nodes popped: a cycle */
+        } else {
+            /* O10 */
+            uint64_t mk = 0, busy = 0;
+            for (uint32_t v = 0; v < NN; v++) { if (end[v] > mk) mk = end[v]; busy += lat[v]; }
+            res->makespan = mk;
+            res->busy = busy;
+            uint64_t den = (uint64_t)P * mk;
+            res->bubble = den ? (double)(den - busy) / (double)den : 0.0;
+            res->status = oom ? ST_OOM : ST_OK;
+            if (tl_start)
+                for (uint32_t v = 0; v < NN; v++) { tl_start[v] = start[v]; tl_end[v] = end[v]; }
+        }
+        free(dir); free(seg); free(lat); free(act); free(slotF); free(slotB);
+        free(esrc); free(edst); free(ew); free(indeg); free(soff); free(sorder); free(fill);
+        free(start); free(end); free(queue);
+    }
+done:
+    free(base); free(W); free(present); free(sb); free(si); free(sj); free(sk);
+}
+
+typedef struct {
+    const oproblem *pb;
+    const ocands *cs;
+    uint64_t lo, hi, first;
+    uint64_t *makespan, *busy, *peaks;
+    uint32_t *status, *oom;
+    double *bubble;
+} job_t;
+
+static void *worker(void *arg) {
+    job_t *j = (job_t *)arg;
+    for (uint64_t x = j->lo; x < j->hi; x++) {
+        ores r;
+        uint64_t o = x - j->first;
+        eval_one(j->pb, j->cs, x, &r, j->peaks ? j->peaks + o * j->pb->P : NULL, NULL, NULL);
+        j->makespan[o] = r.makespan;
+        j->busy[o] = r.busy;
+        j->status[o] = r.status;
+        j->oom[o] = r.oom_mask;
+        j->bubble[o] = r.bubble;
+    }
+    return NULL;
+}
+
+/* Evaluate candidates [first, first+count) of cs (indices into cs arrays). */
+int oracle_eval(const oproblem *pb, const ocands *cs, uint64_t first, uint64_t count,
+                uint64_t *makespan, uint32_t *status, uint32_t *oom_mask, double *bubble,
+                uint64_t *peaks /* [count][P] or NULL */, uint64_t *busy, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 512) threads = 512;
+    if ((uint64_t)threads > count) threads = count ? (int)count : 1;
+    pthread_t th[512];
+    job_t jobs[512];
+    uint64_t per = (count + threads - 1) / threads;
+    for (int t = 0; t < threads; t++) {
+        uint64_t lo = first + per * t, hi = lo + per;
+        if (hi > first + count) hi = first + count;
+        if (lo > hi) lo = hi;
+        jobs[t] = (job_t){pb, cs, lo, hi, first, makespan, busy, peaks, status, oom_mask, bubble};
+        pthread_create(&th[t], NULL, worker, &jobs[t]);
+    }
+    for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+    return 0;
+}
+
+/* Per-(rank, slot) start/end times of candidate x ([P][2n] each); returns the status. */
+int oracle_timeline(const oproblem *pb, const ocands *cs, uint64_t x, uint64_t *tl_start, uint64_t *tl_end) {
+    ores r;
+    eval_one(pb, cs, x, &r, NULL, tl_start, tl_end);
+    return (int)r.status;
+}
+
+/* O11: lowest index among status OK with minimal makespan; returns -1 if none. */
+int64_t oracle_argmin(const uint64_t *makespan, const uint32_t *status, uint64_t count) {
+    int64_t best = -1;
+    for (uint64_t x = 0; x < count; x++)
+        if (status[x] == ST_OK && (best < 0 || makespan[x] < makespan[best])) best = (int64_t)x;
+    return best;
+}
