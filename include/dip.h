@@ -1,0 +1,188 @@
+/* dip.h -- C-ABI of the B200-native DIP candidate-schedule scorer.
+ *
+ * The hot path of DIP (arXiv 2504.14145): for ONE input batch, score a large
+ * batch of candidate pipeline schedules and return the best feasible one.
+ *   - PAPER.md §3.2: per iteration the planner fetches batch
+ *     metadata, builds modality-specific sub-microbatches and searches for the
+ *     schedule with the best score;
+ *   - P:498-499: every rollout "undergoes pipeline stage interleaving ... to
+ *     compute performance scores (i.e., end-to-end iteration time)";
+ *   - P:546-548: memory capacity M per rank must not be exceeded;
+ *   - P:702-705: the simulator "populates operator timestamps in topological
+ *     order, then determines tensor lifetimes ... peak memory usage".
+ * A candidate = a sub-microbatch split M_{b,i} per (microbatch b, module i)
+ * + a shared forward and a shared backward segment sequence + a
+ * per-rank forward/backward interleaving (reading R-1 of DESIGN.md).
+ *
+ * Units: time in integer nanoseconds (u64 accumulators), memory in KiB (u32).
+ * All calls return dip_status (0 = DIP_OK); no C++ exception crosses the ABI.
+ * Per-candidate problems are DATA (dip_result.status), never call errors.
+ * Streams are passed as `void *` holding a cudaStream_t (NULL = legacy default).
+ */
+#ifndef DIP_H
+#define DIP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DIP_OK = 0,
+    DIP_EINVAL = 1,       /* bad argument or malformed problem description */
+    DIP_ECUDA = 2,        /* CUDA runtime error (detail: dip_last_error()) */
+    DIP_ENOMEM = 3,       /* device or host allocation failed */
+    DIP_ERANGE = 4,       /* a load-time overflow guard failed (u32 activations, 2^53 bubble bound) */
+    DIP_ENCCL = 5,        /* NCCL error */
+    DIP_ENOFEASIBLE = 6   /* reserved */
+} dip_status;
+
+/* Per-candidate status, precedence BAD_ENCODING > DEADLOCK > OOM > OK (R-13). */
+typedef enum {
+    DIP_CAND_OK = 0,
+    DIP_CAND_OOM = 1,           /* timed; some rank's peak > its budget (strict >, R-10) */
+    DIP_CAND_DEADLOCK = 2,      /* the stage x slot dependency graph has a cycle (R-12) */
+    DIP_CAND_BAD_ENCODING = 3   /* malformed candidate (R-11) */
+} dip_cand_status;
+
+/* One modality module. Tables are per LAYER, indexed by the work W of a
+ * sub-microbatch (W = sum of its instances' work units, R-21), W in [0, w_max]. */
+typedef struct {
+    uint32_t L;               /* layers */
+    uint32_t K;               /* pipeline segments; the module has P*K chunks */
+    uint32_t max_split;       /* M_max in [1, 15]: candidates choose M in [1, min(N, M_max)] (R-2) */
+    uint32_t w_max;           /* tables have w_max + 1 entries */
+    uint32_t producer_mask;   /* bit p: module p (p < this module's index) feeds this one (R-5) */
+    const uint32_t *chunk_layers; /* NULL (default: P*K chunks of consecutive layers, remainder to
+                                     the earliest, R-3) or [P*K] explicit layers per chunk */
+    const uint32_t *f_ns;     /* [w_max+1] forward ns per layer */
+    const uint32_t *b_ns;     /* [w_max+1] backward ns per layer */
+    const uint32_t *act_kib;  /* [w_max+1] activation KiB per layer, held from F start to B end (R-9) */
+    const uint32_t *p2p_ns;   /* [w_max+1] boundary transfer ns on cross-rank edges (R-7); NULL = 0 */
+} dip_module_desc;
+
+/* Problem = model partition + per-layer cost tables + batch metadata. */
+typedef struct {
+    uint32_t P;               /* pipeline ranks, 1..32 */
+    uint32_t n_modules;       /* 1..8, in topological order (producers first) */
+    uint32_t m;               /* microbatches, 1..255 */
+    const dip_module_desc *modules;
+    const uint32_t *inst_off; /* [m*n_modules+1] b-major offsets into inst_units: (b,i) owns
+                                 instances [inst_off[b*n+i], inst_off[b*n+i+1]) in packing order */
+    const uint16_t *inst_units; /* per-instance work units */
+    const uint32_t *budget_kib; /* [P] activation budget per rank (capacity - static), KiB */
+} dip_problem_desc;
+
+typedef struct dip_model dip_model;           /* opaque, library-owned, immutable after load */
+typedef struct dip_workspace dip_workspace;   /* opaque per-stream scratch (work queue, argmin key, spill) */
+typedef struct dip_comm dip_comm;             /* opaque NCCL communicator */
+
+typedef struct {
+    uint32_t P, n_modules, m;
+    uint32_t n_max;           /* segment-id space: id(b,i,j,k) = base(b,i) + j*K_i + k (b-major) */
+    uint32_t fbw;             /* 32-bit words per rank of F/B bits: ceil(2*n_max/32) */
+    uint32_t record_stride;   /* bytes per packed candidate record (multiple of 16) */
+    uint32_t group_lanes;     /* lanes per candidate in the kernel (power of two >= P) */
+    uint32_t smem_per_block;  /* dynamic shared memory of the scoring kernel */
+    uint32_t warps_per_block, blocks_per_sm, grid;
+    uint64_t makespan_bound;  /* load-time upper bound on any makespan (overflow guards) */
+} dip_model_info;
+
+/* cuda_device < 0 gives a host-only model (encoding, validation, dip_model_get_info).
+ * Validate the problem, derive the segment-decode table, layers per chunk, the
+ * balanced-split work table (R-2) and copy them to `cuda_device`.
+ * The descriptor is read only during the call. Errors: DIP_EINVAL (P not in
+ * 1..32, P*K > L without chunk_layers, producer_mask not topological, M_max > 15,
+ * ...), DIP_ERANGE (a (b,i) total work exceeds w_max, or an overflow guard),
+ * DIP_ECUDA, DIP_ENOMEM. */
+dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_model **out);
+dip_status dip_model_free(dip_model *m);
+dip_status dip_model_get_info(const dip_model *m, dip_model_info *out);
+
+/* Host view of `count` candidates (struct of arrays, row-major):
+ *   split   u8  [count][m*n_modules]  M_{b,i}
+ *   n       u32 [count]               number of forward segments
+ *   fwd_seq u16 [count][n_max]        segment ids in forward order, pad 0xFFFF
+ *   bwd_seq u16 [count][n_max]        segment ids in backward order, pad 0xFFFF
+ *   fb_bits u32 [count][P][fbw]       rank r, slot t: bit t%32 of word t/32; 1 = next backward
+ * Rank r's slot t runs the next unread fwd_seq entry (bit 0) or bwd_seq entry (bit 1). */
+typedef struct {
+    const uint8_t *split;
+    const uint32_t *n;
+    const uint16_t *fwd_seq, *bwd_seq;
+    const uint32_t *fb_bits;
+} dip_candidate_batch;
+
+/* Pack candidates into records of info.record_stride bytes (HOST memory, e.g. pinned),
+ * the layout dip_eval_schedules reads:
+ *   off 0   u16 n, u16 flags (bit 0: encoding unrepresentable -> BAD_ENCODING)
+ *   off 4   u8  nibbles: M_{b,i} for the modules with M_max > 1, b-major
+ *   off A   u16 fwd[n_pad], then u16 bwd[n_pad]   (n_pad = n_max rounded up to 8; pad 0xFFFF)
+ *   off C   u32 fb[fbw][P]   (word-major: the P lanes of a candidate read one 4P-byte row)
+ * Unrepresentable inputs (n > n_max, split > 15, ...) set flag bit 0 so that the
+ * kernel reports BAD_ENCODING exactly like the oracle. threads <= 0: all cores. */
+dip_status dip_encode_candidates(const dip_model *m, const dip_candidate_batch *c, size_t count,
+                                 void *out_records, int threads);
+
+/* 24-byte result per candidate. BAD_ENCODING/DEADLOCK: makespan = UINT64_MAX,
+ * bubble = -1.0. bubble = (P*makespan - sum of busy ns) / (P*makespan) as one IEEE
+ * double division of exact integers (R-16); 0.0 when P*makespan = 0. */
+typedef struct {
+    uint64_t makespan_ns;
+    uint32_t status;          /* dip_cand_status */
+    uint32_t oom_mask;        /* bit r: peak_r > budget_r */
+    double bubble;
+} dip_result;
+
+/* Per-stream scratch: work-queue counter, fused argmin key, spill area for the
+ * DP's inter-rank channels, and (if host_chunk > 0) double-buffered device
+ * staging of host_chunk records for dip_eval_host. */
+dip_status dip_workspace_create(const dip_model *m, size_t host_chunk, dip_workspace **out);
+dip_status dip_workspace_free(dip_workspace *w);
+
+/* Score `count` device-resident records (d_records, count*stride bytes) on `stream`:
+ * decode + cost lookup + longest-path DP + memory peaks + bubble, and the fused
+ * argmin epilogue into the workspace key. Asynchronous. d_results: [count] device;
+ * d_peaks_kib: [count][P] device or NULL. Candidate i's index is i (local). */
+dip_status dip_eval_schedules(const dip_model *m, dip_workspace *w, const void *d_records, size_t count,
+                              dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+
+typedef struct {
+    int32_t found;            /* 0 if no candidate has status OK on any rank */
+    int32_t rank;             /* owning rank */
+    uint64_t global_index;    /* rank * shard_stride + local index (contiguous shards) */
+    uint64_t makespan_ns;
+} dip_winner;
+
+/* Lowest (makespan, global index) among status-OK candidates of the last
+ * dip_eval_schedules/dip_eval_host on `w` (R-15), reduced over `world` ranks with
+ * one ncclAllReduce(MIN) of a packed (makespan, rank, index) u64 key on `stream`
+ * (comm may be NULL when world == 1). Synchronous: returns after the host has the
+ * winner. shard_stride = candidates per rank shard (>= count). */
+dip_status dip_argmin(const dip_model *m, dip_workspace *w, size_t count, uint64_t shard_stride,
+                      uint32_t rank, uint32_t world, dip_comm *comm, dip_winner *out, void *stream);
+
+/* End to end from HOST records (pinned for overlap): chunked H2D copies overlapped
+ * with scoring, then dip_argmin. h_results ([count], host) may be NULL. Requires a
+ * workspace created with host_chunk > 0. Synchronous. */
+dip_status dip_eval_host(const dip_model *m, dip_workspace *w, const void *h_records, size_t count,
+                         dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world,
+                         dip_comm *comm, dip_winner *out, void *stream);
+
+/* NCCL communicator for the argmin: rank 0 calls dip_comm_unique_id, broadcasts
+ * the 128 bytes (e.g. over torch.distributed), every rank calls dip_comm_init. */
+dip_status dip_comm_unique_id(uint8_t id_out[128]);
+dip_status dip_comm_init(const uint8_t id[128], int rank, int world, int cuda_device, dip_comm **out);
+dip_status dip_comm_free(dip_comm *c);
+
+/* Number of kernel launches issued by this process so far (the scorer's own kernels). */
+uint64_t dip_launch_count(void);
+const char *dip_status_str(dip_status s);
+const char *dip_last_error(void);   /* thread-local detail of the last failing call */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIP_H */

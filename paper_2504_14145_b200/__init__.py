@@ -1,0 +1,7 @@
+"""B200-native (sm_100a) DIP candidate-schedule scorer (arXiv 2504.14145).
+
+The product is libdip.so (include/dip.h): hand-written CUDA kernels behind a C-ABI.
+This package only builds it (build.py) and binds it (dip.py).
+"""
+from .dip import (CAND_BAD, CAND_DEADLOCK, CAND_OK, CAND_OOM, RESULT_DTYPE, Comm, DipError, Model,  # noqa: F401
+                  Winner, Workspace, argmin, eval_host, eval_schedules, launch_count, lib, results_view)

@@ -1,0 +1,630 @@
+// dip_host.cpp -- the C-ABI (include/dip.h): batch setup, candidate packing, launches,
+// argmin with the NCCL allreduce, and the end-to-end host path.
+//
+// (a1) batch setup: derive layers per chunk (R-3),
+//      the segment-id decode table, per (microbatch, module) the balanced-split work
+//      table W_j for every M in [1, M_max] (R-2), the per-layer cost rows, and
+//      pack them into one 16-B aligned blob that the kernel stages into shared memory
+//      with a TMA bulk copy.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "dip.h"
+#include "dip_internal.h"
+
+using dipk::KParams;
+using dipk::ModInfo;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+dip_status fail(dip_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+#define CUDA_TRY(x)                                                                            \
+    do {                                                                                       \
+        cudaError_t _e = (x);                                                                  \
+        if (_e != cudaSuccess) return fail(DIP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+#define NCCL_TRY(x)                                                                            \
+    do {                                                                                       \
+        ncclResult_t _r = (x);                                                                 \
+        if (_r != ncclSuccess) return fail(DIP_ENCCL, std::string(#x) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+inline uint32_t up16(uint32_t x) { return (x + 15u) & ~15u; }
+inline uint32_t bits_for(uint64_t n) {   // smallest b >= 1 with n <= 2^b
+    uint32_t b = 1;
+    while (b < 63 && (1ull << b) < n) b++;
+    return b;
+}
+
+}  // namespace
+
+struct dip_model {
+    int device = 0;
+    uint32_t P = 0, nmod = 0, m = 0, n_max = 0, n_pad = 0, fbw = 0, stride = 0;
+    uint32_t off_nib = 0, off_fwd = 0, off_bwd = 0, off_fb = 0, nsplit = 0;
+    std::vector<uint32_t> max_split, nib_slot, nbi;   // host copies for encode
+    std::vector<uint8_t> blob;
+    uint8_t *d_blob = nullptr;
+    KParams kp{};                  // shape + blob + layout; per-launch fields filled per call
+    int G = 32, cpg = 1, wpb = 1, bps = 1, grid = 1, num_sms = 148;
+    size_t smem = 0;
+    uint64_t mk_bound = 0;
+};
+
+struct dip_workspace {
+    const dip_model *model = nullptr;
+    unsigned long long *d_misc = nullptr;   // [0] counter [1] key [2] gkey [3] mk [4] idx [5..] spare
+    unsigned long long *h_misc = nullptr;   // pinned
+    unsigned long long *d_spill = nullptr;
+    size_t spill_bytes = 0;
+    // last eval
+    const dip_result *last_results = nullptr;
+    uint64_t last_count = 0;
+    uint32_t last_idx_bits = 1;
+    bool last_fused = true;
+    // host path
+    size_t host_chunk = 0;
+    uint8_t *d_rec[2] = {nullptr, nullptr};
+    dip_result *d_res = nullptr;           // [count capacity] grows on demand? fixed: 2 * host_chunk
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+};
+
+struct dip_comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+static void fill_shape(dip_model *M) {
+    KParams &kp = M->kp;
+    kp.P = M->P; kp.nmod = M->nmod; kp.m = M->m; kp.n_max = M->n_max; kp.n_pad = M->n_pad; kp.fbw = M->fbw;
+    kp.stride = M->stride;
+    kp.off_nib = M->off_nib; kp.off_fwd = M->off_fwd; kp.off_bwd = M->off_bwd; kp.off_fb = M->off_fb;
+    kp.nsplit = M->nsplit;
+    kp.warps_per_block = M->wpb;
+    kp.cpg = M->cpg;
+}
+
+extern "C" {
+
+const char *dip_status_str(dip_status s) {
+    switch (s) {
+    case DIP_OK: return "DIP_OK";
+    case DIP_EINVAL: return "DIP_EINVAL";
+    case DIP_ECUDA: return "DIP_ECUDA";
+    case DIP_ENOMEM: return "DIP_ENOMEM";
+    case DIP_ERANGE: return "DIP_ERANGE";
+    case DIP_ENCCL: return "DIP_ENCCL";
+    case DIP_ENOFEASIBLE: return "DIP_ENOFEASIBLE";
+    }
+    return "DIP_?";
+}
+const char *dip_last_error(void) { return g_err.c_str(); }
+uint64_t dip_launch_count(void) { return g_launches.load(); }
+
+dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_model **out) {
+    if (!d || !out || !d->modules || !d->inst_off || !d->budget_kib) return fail(DIP_EINVAL, "null argument");
+    const uint32_t P = d->P, nm = d->n_modules, m = d->m;
+    if (P < 1 || P > 32) return fail(DIP_EINVAL, "P must be in 1..32");
+    if (nm < 1 || nm > 8) return fail(DIP_EINVAL, "n_modules must be in 1..8");
+    if (m < 1 || m > 255) return fail(DIP_EINVAL, "m must be in 1..255");
+    dip_model *M = new (std::nothrow) dip_model();
+    if (!M) return fail(DIP_ENOMEM, "host allocation");
+    std::unique_ptr<dip_model> guard(M);
+    M->device = cuda_device;
+    M->P = P; M->nmod = nm; M->m = m;
+
+    // ---- per module: chunks (R-3), consumers, table offsets
+    std::vector<ModInfo> mi(nm);
+    std::vector<uint16_t> layers;
+    std::vector<uint32_t> tab;   // 4 x u32 per entry
+    uint32_t maxlat_layers = 0;
+    uint64_t maxlat = 0, maxp2p = 0, maxact = 0;
+    uint32_t nsplit = 0;
+    for (uint32_t i = 0; i < nm; i++) {
+        const dip_module_desc &md = d->modules[i];
+        if (md.K < 1 || md.K > 255) return fail(DIP_EINVAL, "K must be in 1..255");
+        if (md.max_split < 1 || md.max_split > 15) return fail(DIP_EINVAL, "max_split must be in 1..15");
+        if (!md.f_ns || !md.b_ns || !md.act_kib) return fail(DIP_EINVAL, "null cost table");
+        if (md.producer_mask >> i) return fail(DIP_EINVAL, "producer_mask must name earlier modules only");
+        const uint32_t C = P * md.K;
+        if (!md.chunk_layers && C > md.L) return fail(DIP_EINVAL, "P*K > L (TooManyChunks)");
+        ModInfo &x = mi[i];
+        x.K = md.K;
+        x.max_split = md.max_split;
+        x.prod_mask = md.producer_mask;
+        x.cons_mask = 0;
+        for (uint32_t c = 0; c < nm; c++)
+            if ((d->modules[c].producer_mask >> i) & 1u) x.cons_mask |= 1u << c;
+        x.lay_off = (uint32_t)layers.size();
+        for (uint32_t c = 0; c < C; c++) {
+            const uint32_t l = md.chunk_layers ? md.chunk_layers[c] : md.L / C + (c < md.L % C ? 1u : 0u);
+            if (l > 65535) return fail(DIP_ERANGE, "layers per chunk > 65535");
+            layers.push_back((uint16_t)l);
+            maxlat_layers = std::max(maxlat_layers, l);
+        }
+        x.tab_off = (uint32_t)(tab.size() / 4);
+        x.w_max = md.w_max;
+        for (uint32_t w = 0; w <= md.w_max; w++) {
+            const uint32_t p2p = (md.p2p_ns && P > 1) ? md.p2p_ns[w] : 0u;   // P = 1: no cross-rank edge
+            tab.push_back(md.f_ns[w]);
+            tab.push_back(md.b_ns[w]);
+            tab.push_back(md.act_kib[w]);
+            tab.push_back(p2p);
+            maxlat = std::max<uint64_t>(maxlat, std::max(md.f_ns[w], md.b_ns[w]));
+            maxact = std::max<uint64_t>(maxact, md.act_kib[w]);
+            maxp2p = std::max<uint64_t>(maxp2p, p2p);
+        }
+        x.nib_slot = md.max_split > 1 ? nsplit++ : 0xFFu;
+        M->max_split.push_back(md.max_split);
+        M->nib_slot.push_back(x.nib_slot);
+    }
+    if (tab.size() / 4 > 65535 || layers.size() > 65535) return fail(DIP_ERANGE, "tables too large");
+
+    // ---- segment ids, decode table, per-(b,i) base, balanced-split work table (R-2)
+    uint32_t n_max = 0;
+    std::vector<uint16_t> sbase(m * nm);
+    std::vector<uint32_t> segdec;
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            sbase[b * nm + i] = (uint16_t)n_max;
+            for (uint32_t j = 0; j < mi[i].max_split; j++)
+                for (uint32_t k = 0; k < mi[i].K; k++) segdec.push_back(dipk::segdec_pack(b, i, j, k, mi[i].K));
+            n_max += mi[i].max_split * mi[i].K;
+            if (n_max > 65534) return fail(DIP_ERANGE, "segment-id space exceeds 65534");
+        }
+    std::vector<uint32_t> woff(m * nm);
+    std::vector<uint16_t> wtab, nbi(m * nm);
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            const uint32_t q = b * nm + i, lo = d->inst_off[q], hi = d->inst_off[q + 1];
+            if (hi < lo) return fail(DIP_EINVAL, "inst_off must be non-decreasing");
+            const uint32_t N = hi - lo;
+            if (N > 65535) return fail(DIP_ERANGE, "too many instances");
+            nbi[q] = (uint16_t)N;
+            M->nbi.push_back(N);
+            woff[q] = (uint32_t)wtab.size();
+            uint64_t total = 0;
+            for (uint32_t u = lo; u < hi; u++) total += d->inst_units[u];
+            if (total > mi[i].w_max) return fail(DIP_ERANGE, "a (microbatch, module) work exceeds w_max");
+            for (uint32_t Ms = 1; Ms <= mi[i].max_split; Ms++) {
+                // part j covers instances [j*q + min(j,rho), (j+1)*q + min(j+1,rho)) (balanced, contiguous)
+                const uint32_t qq = Ms ? N / Ms : 0, rho = Ms ? N % Ms : 0;
+                for (uint32_t j = 0; j < Ms; j++) {
+                    const uint32_t a = j * qq + std::min(j, rho), e = (j + 1) * qq + std::min(j + 1, rho);
+                    uint32_t w = 0;
+                    for (uint32_t u = a; u < e; u++) w += d->inst_units[lo + u];
+                    wtab.push_back((uint16_t)w);
+                }
+            }
+        }
+
+    // ---- overflow guards (DIP_ERANGE)
+    const uint64_t nodes = (uint64_t)P * 2ull * n_max;
+    const unsigned __int128 bound = (unsigned __int128)nodes * ((unsigned __int128)maxlat_layers * maxlat + maxp2p);
+    if (bound * P >= ((unsigned __int128)1 << 53)) return fail(DIP_ERANGE, "makespan bound exceeds 2^53 / P");
+    if ((unsigned __int128)n_max * maxlat_layers * maxact >= ((unsigned __int128)1 << 32))
+        return fail(DIP_ERANGE, "per-rank activation sum may exceed u32 KiB");
+    M->mk_bound = (uint64_t)bound;
+
+    // ---- blob (16-B aligned sections)
+    std::vector<uint8_t> &blob = M->blob;
+    auto put = [&](const void *src, size_t bytes) {
+        const uint32_t off = up16((uint32_t)blob.size());
+        blob.resize(off + bytes);
+        if (bytes) std::memcpy(blob.data() + off, src, bytes);
+        return off;
+    };
+    KParams &kp = M->kp;
+    kp.b_modinfo = put(mi.data(), mi.size() * sizeof(ModInfo));
+    kp.b_tab = put(tab.data(), tab.size() * 4);
+    kp.b_segdec = put(segdec.data(), segdec.size() * 4);
+    kp.b_woff = put(woff.data(), woff.size() * 4);
+    kp.b_layers = put(layers.data(), layers.size() * 2);
+    kp.b_wtab = put(wtab.data(), wtab.size() * 2);
+    kp.b_nbi = put(nbi.data(), nbi.size() * 2);
+    kp.b_sbase = put(sbase.data(), sbase.size() * 2);
+    kp.b_budget = put(d->budget_kib, P * 4);
+    blob.resize(up16((uint32_t)blob.size()));
+    kp.blob_bytes = (uint32_t)blob.size();
+
+    // ---- record layout
+    M->n_max = n_max;
+    M->n_pad = (n_max + 7) & ~7u;
+    M->fbw = std::max<uint32_t>(1, (2 * n_max + 31) / 32);
+    M->nsplit = nsplit;
+    M->off_nib = 4;
+    M->off_fwd = up16(4 + (m * nsplit + 1) / 2);
+    M->off_bwd = M->off_fwd + 2 * M->n_pad;
+    M->off_fb = up16(M->off_bwd + 2 * M->n_pad);
+    M->stride = up16(M->off_fb + 4 * M->fbw * P);
+
+    // ---- kernel shape: group of G lanes per candidate, per-group smem working set
+    int G = 4;
+    while (G < (int)P) G *= 2;
+    M->G = G;
+    M->cpg = 32 / G;
+    uint32_t go = 0;
+    auto gput = [&](uint32_t bytes) { const uint32_t o = go; go = up16(go + bytes); return o; };
+    kp.g_seqF = gput(2 * M->n_pad);
+    kp.g_seqB = gput(2 * M->n_pad);
+    kp.g_posF = gput(4 * n_max);
+    kp.g_posB = gput(4 * n_max);
+    kp.g_depF0 = gput(8 * n_max);
+    kp.g_depBP = gput(std::max<uint32_t>(8 * n_max, 8 * ((n_max + 31) / 32)));
+    kp.g_ring = gput(std::max<uint32_t>(2 * P * dipk::RING_D * 8, 4 * n_max));
+    kp.g_bmf = gput(3 * m * nm);
+    kp.g_bytes = go;
+
+    if (cuda_device < 0) {   // host-only model: encoding and validation, no device resources
+        *out = guard.release();
+        fill_shape(*out);
+        return DIP_OK;
+    }
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, cuda_device));
+    M->num_sms = prop.multiProcessorCount;
+    const size_t smem_cap = prop.sharedMemPerBlockOptin;
+    const size_t per_warp = (size_t)M->cpg * kp.g_bytes;
+    int best_w = 0, best_wpb = 0, best_bps = 0;
+    size_t best_smem = 0;
+    for (int wpb = 1; wpb <= 8; wpb++) {
+        const size_t sm = kp.blob_bytes + wpb * per_warp;
+        if (sm > smem_cap) break;
+        CUDA_TRY(dipk::prepare_eval(G, sm));
+        int bps = 0;
+        CUDA_TRY(dipk::occupancy_eval(G, wpb * 32, sm, &bps));
+        if (bps < 1) continue;
+        if (wpb * bps >= best_w) { best_w = wpb * bps; best_wpb = wpb; best_bps = bps; best_smem = sm; }
+    }
+    if (!best_w) return fail(DIP_ERANGE, "per-candidate working set does not fit in shared memory");
+    M->wpb = best_wpb;
+    M->bps = best_bps;
+    M->smem = best_smem;
+    M->grid = M->num_sms * best_bps;
+    CUDA_TRY(dipk::prepare_eval(G, best_smem));
+
+    CUDA_TRY(cudaMalloc(&M->d_blob, kp.blob_bytes));
+    CUDA_TRY(cudaMemcpy(M->d_blob, blob.data(), kp.blob_bytes, cudaMemcpyHostToDevice));
+    kp.blob = M->d_blob;
+    fill_shape(M);
+    *out = guard.release();
+    return DIP_OK;
+}
+
+dip_status dip_model_free(dip_model *m) {
+    if (!m) return DIP_OK;
+    if (m->d_blob) cudaFree(m->d_blob);
+    delete m;
+    return DIP_OK;
+}
+
+dip_status dip_model_get_info(const dip_model *m, dip_model_info *o) {
+    if (!m || !o) return fail(DIP_EINVAL, "null argument");
+    o->P = m->P; o->n_modules = m->nmod; o->m = m->m; o->n_max = m->n_max; o->fbw = m->fbw;
+    o->record_stride = m->stride; o->group_lanes = (uint32_t)m->G; o->smem_per_block = (uint32_t)m->smem;
+    o->warps_per_block = (uint32_t)m->wpb; o->blocks_per_sm = (uint32_t)m->bps; o->grid = (uint32_t)m->grid;
+    o->makespan_bound = m->mk_bound;
+    return DIP_OK;
+}
+
+// ---------------------------------------------------------------- encode (host) --------
+static void encode_range(const dip_model *M, const dip_candidate_batch *c, size_t lo, size_t hi, uint8_t *out) {
+    const uint32_t P = M->P, nm = M->nmod, m = M->m, n_max = M->n_max, fbw = M->fbw;
+    for (size_t x = lo; x < hi; x++) {
+        uint8_t *rec = out + x * M->stride;
+        std::memset(rec, 0, M->stride);
+        const uint32_t n = c->n[x];
+        uint16_t flags = 0;
+        if (n > n_max || n > 65535) flags |= 1;
+        const uint16_t nh = (uint16_t)std::min<uint32_t>(n, 65535);
+        std::memcpy(rec, &nh, 2);
+        const uint8_t *sp = c->split + x * (size_t)m * nm;
+        for (uint32_t b = 0; b < m; b++)
+            for (uint32_t i = 0; i < nm; i++) {
+                const uint32_t v = sp[b * nm + i];
+                if (M->max_split[i] > 1) {
+                    if (v > 15) flags |= 1;
+                    const uint32_t nib = b * M->nsplit + M->nib_slot[i];
+                    rec[M->off_nib + nib / 2] |= (uint8_t)((v & 15u) << ((nib & 1) * 4));
+                } else if (v != (M->nbi[b * nm + i] > 0 ? 1u : 0u)) {
+                    flags |= 1;   // unrepresentable: the implied value is the only valid one
+                }
+            }
+        std::memcpy(rec + 2, &flags, 2);
+        uint16_t *fw = reinterpret_cast<uint16_t *>(rec + M->off_fwd);
+        uint16_t *bw = reinterpret_cast<uint16_t *>(rec + M->off_bwd);
+        std::memcpy(fw, c->fwd_seq + x * (size_t)n_max, 2 * n_max);
+        std::memcpy(bw, c->bwd_seq + x * (size_t)n_max, 2 * n_max);
+        for (uint32_t p = n_max; p < M->n_pad; p++) { fw[p] = 0xFFFF; bw[p] = 0xFFFF; }
+        uint32_t *fb = reinterpret_cast<uint32_t *>(rec + M->off_fb);
+        const uint32_t *src = c->fb_bits + x * (size_t)P * fbw;
+        for (uint32_t r = 0; r < P; r++)
+            for (uint32_t w = 0; w < fbw; w++) fb[w * P + r] = src[r * fbw + w];
+    }
+}
+
+dip_status dip_encode_candidates(const dip_model *M, const dip_candidate_batch *c, size_t count, void *out,
+                                 int threads) {
+    if (!M || !c || (!out && count)) return fail(DIP_EINVAL, "null argument");
+    if (!count) return DIP_OK;
+    if (!c->split || !c->n || !c->fwd_seq || !c->bwd_seq || !c->fb_bits) return fail(DIP_EINVAL, "null array");
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    threads = (int)std::min<size_t>(threads, std::max<size_t>(1, count / 256));
+    std::vector<std::thread> th;
+    const size_t per = (count + threads - 1) / threads;
+    for (int t = 0; t < threads; t++) {
+        const size_t lo = per * t, hi = std::min(count, lo + per);
+        if (lo >= hi) break;
+        th.emplace_back(encode_range, M, c, lo, hi, static_cast<uint8_t *>(out));
+    }
+    for (auto &t : th) t.join();
+    return DIP_OK;
+}
+
+// ---------------------------------------------------------------- workspace ------------
+dip_status dip_workspace_create(const dip_model *M, size_t host_chunk, dip_workspace **out) {
+    if (!M || !out) return fail(DIP_EINVAL, "null argument");
+    if (M->device < 0 || !M->d_blob) return fail(DIP_EINVAL, "host-only model (cuda_device < 0)");
+    CUDA_TRY(cudaSetDevice(M->device));
+    dip_workspace *w = new (std::nothrow) dip_workspace();
+    if (!w) return fail(DIP_ENOMEM, "host allocation");
+    std::unique_ptr<dip_workspace> guard(w);
+    w->model = M;
+    CUDA_TRY(cudaMalloc(&w->d_misc, 16 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(w->d_misc, 0, 16 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMallocHost(&w->h_misc, 16 * sizeof(unsigned long long)));
+    const size_t slots = (size_t)M->grid * M->wpb * M->cpg;
+    w->spill_bytes = slots * 2ull * M->P * M->n_max * sizeof(unsigned long long);
+    CUDA_TRY(cudaMalloc(&w->d_spill, w->spill_bytes));
+    w->host_chunk = host_chunk;
+    if (host_chunk) {
+        for (int b = 0; b < 2; b++) {
+            CUDA_TRY(cudaMalloc(&w->d_rec[b], host_chunk * M->stride));
+            CUDA_TRY(cudaEventCreateWithFlags(&w->ev_copied[b], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&w->ev_free[b], cudaEventDisableTiming));
+        }
+        CUDA_TRY(cudaMalloc(&w->d_res, 2 * host_chunk * sizeof(dip_result)));
+        CUDA_TRY(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+    }
+    *out = guard.release();
+    return DIP_OK;
+}
+
+dip_status dip_workspace_free(dip_workspace *w) {
+    if (!w) return DIP_OK;
+    if (w->d_misc) cudaFree(w->d_misc);
+    if (w->h_misc) cudaFreeHost(w->h_misc);
+    if (w->d_spill) cudaFree(w->d_spill);
+    for (int b = 0; b < 2; b++) {
+        if (w->d_rec[b]) cudaFree(w->d_rec[b]);
+        if (w->ev_copied[b]) cudaEventDestroy(w->ev_copied[b]);
+        if (w->ev_free[b]) cudaEventDestroy(w->ev_free[b]);
+    }
+    if (w->d_res) cudaFree(w->d_res);
+    if (w->copy_stream) cudaStreamDestroy(w->copy_stream);
+    delete w;
+    return DIP_OK;
+}
+
+// ---------------------------------------------------------------- eval -----------------
+static dip_status launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
+                               uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
+                               uint32_t *d_peaks, cudaStream_t s) {
+    KParams kp = M->kp;
+    kp.records = static_cast<const uint8_t *>(d_records);
+    kp.count = count;
+    kp.index_base = index_base;
+    kp.results = d_results;
+    kp.peaks = d_peaks;
+    kp.counter = w->d_misc + 0;
+    kp.best_key = w->d_misc + 1;
+    kp.spill = w->d_spill;
+    kp.fused_key = fused ? 1u : 0u;
+    kp.idx_bits = idx_bits;
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 0, 0, sizeof(unsigned long long), s));
+    const int grid = (int)std::min<uint64_t>((uint64_t)M->grid,
+                                             std::max<uint64_t>(1, (count + M->cpg * M->wpb - 1) / (M->cpg * M->wpb)));
+    CUDA_TRY(dipk::launch_eval(kp, M->G, grid, M->wpb * 32, M->smem, s));
+    g_launches++;
+    return DIP_OK;
+}
+
+static bool fused_ok(const dip_model *M, uint32_t idx_bits) {
+    return idx_bits < 63 && (M->mk_bound >> (64 - idx_bits)) == 0;
+}
+
+dip_status dip_eval_schedules(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
+                              dip_result *d_results, uint32_t *d_peaks, void *stream) {
+    if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
+    if (count && (!d_records || !d_results)) return fail(DIP_EINVAL, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t idx_bits = bits_for(std::max<uint64_t>(count, 2));
+    const bool fused = fused_ok(M, idx_bits);
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
+    w->last_results = d_results;
+    w->last_count = count;
+    w->last_idx_bits = idx_bits;
+    w->last_fused = fused;
+    if (!count) return DIP_OK;
+    return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s);
+}
+
+// local winner -> (makespan, local index) on the host; exact two-pass scan when not fused
+static dip_status local_best(const dip_model *M, dip_workspace *w, cudaStream_t s, uint64_t *mk, uint64_t *idx,
+                             bool *found) {
+    if (w->last_fused) {
+        CUDA_TRY(cudaMemcpyAsync(w->h_misc, w->d_misc + 1, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const unsigned long long k = w->h_misc[0];
+        *found = k != ~0ull;
+        *mk = *found ? k >> w->last_idx_bits : ~0ull;
+        *idx = *found ? k & ((1ull << w->last_idx_bits) - 1) : ~0ull;
+        return DIP_OK;
+    }
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 3, 0xFF, 16, s));
+    if (w->last_count) {
+        CUDA_TRY(dipk::launch_scan_argmin(w->last_results, w->last_count, 0, w->d_misc + 3, nullptr, s));
+        CUDA_TRY(dipk::launch_scan_argmin_idx(w->last_results, w->last_count, 0, w->d_misc + 3, w->d_misc + 4, s));
+        g_launches += 2;
+    }
+    CUDA_TRY(cudaMemcpyAsync(w->h_misc, w->d_misc + 3, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *found = w->h_misc[0] != ~0ull;
+    *mk = w->h_misc[0];
+    *idx = w->h_misc[1];
+    return DIP_OK;
+}
+
+dip_status dip_argmin(const dip_model *M, dip_workspace *w, size_t count, uint64_t shard_stride, uint32_t rank,
+                      uint32_t world, dip_comm *comm, dip_winner *out, void *stream) {
+    if (!M || !w || !out) return fail(DIP_EINVAL, "null argument");
+    if (world < 1 || rank >= world || (world > 1 && !comm)) return fail(DIP_EINVAL, "bad rank/world/comm");
+    if (count != w->last_count) return fail(DIP_EINVAL, "count differs from the last eval on this workspace");
+    if (shard_stride < count) return fail(DIP_EINVAL, "shard_stride < count");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::memset(out, 0, sizeof(*out));
+    if (world == 1) {
+        uint64_t mk, idx;
+        bool found;
+        dip_status st = local_best(M, w, s, &mk, &idx, &found);
+        if (st != DIP_OK) return st;
+        out->found = found;
+        out->rank = 0;
+        out->global_index = found ? idx : ~0ull;
+        out->makespan_ns = mk;
+        return DIP_OK;
+    }
+    const uint32_t ibits = bits_for(std::max<uint64_t>(shard_stride, 2)), rbits = bits_for(std::max<uint32_t>(world, 2));
+    const bool packed = w->last_fused && ibits + rbits < 63 && (M->mk_bound >> (64 - ibits - rbits)) == 0;
+    if (packed) {
+        // one allreduce of the packed (makespan, rank, local index) key
+        CUDA_TRY(dipk::launch_make_gkey(w->d_misc + 1, w->d_misc + 2, w->last_idx_bits, ibits, rbits, rank, s));
+        g_launches++;
+        NCCL_TRY(ncclAllReduce(w->d_misc + 2, w->d_misc + 2, 1, ncclUint64, ncclMin, comm->comm, s));
+        CUDA_TRY(cudaMemcpyAsync(w->h_misc, w->d_misc + 2, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const unsigned long long k = w->h_misc[0];
+        out->found = k != ~0ull;
+        if (out->found) {
+            const uint64_t local = k & ((1ull << ibits) - 1);
+            out->rank = (int32_t)((k >> ibits) & ((1ull << rbits) - 1));
+            out->makespan_ns = k >> (ibits + rbits);
+            out->global_index = (uint64_t)out->rank * shard_stride + local;
+        } else {
+            out->rank = -1;
+            out->makespan_ns = ~0ull;
+            out->global_index = ~0ull;
+        }
+        return DIP_OK;
+    }
+    // exact fallback: min makespan, then min global index among ties (two allreduces)
+    uint64_t mk, idx;
+    bool found;
+    dip_status st = local_best(M, w, s, &mk, &idx, &found);
+    if (st != DIP_OK) return st;
+    w->h_misc[2] = found ? mk : ~0ull;
+    CUDA_TRY(cudaMemcpyAsync(w->d_misc + 5, w->h_misc + 2, 8, cudaMemcpyHostToDevice, s));
+    NCCL_TRY(ncclAllReduce(w->d_misc + 5, w->d_misc + 5, 1, ncclUint64, ncclMin, comm->comm, s));
+    CUDA_TRY(cudaMemcpyAsync(w->h_misc + 3, w->d_misc + 5, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const uint64_t gmk = w->h_misc[3];
+    w->h_misc[4] = (found && mk == gmk) ? (uint64_t)rank * shard_stride + idx : ~0ull;
+    CUDA_TRY(cudaMemcpyAsync(w->d_misc + 6, w->h_misc + 4, 8, cudaMemcpyHostToDevice, s));
+    NCCL_TRY(ncclAllReduce(w->d_misc + 6, w->d_misc + 6, 1, ncclUint64, ncclMin, comm->comm, s));
+    CUDA_TRY(cudaMemcpyAsync(w->h_misc + 5, w->d_misc + 6, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    out->found = gmk != ~0ull;
+    out->makespan_ns = gmk;
+    out->global_index = w->h_misc[5];
+    out->rank = out->found ? (int32_t)(w->h_misc[5] / shard_stride) : -1;
+    return DIP_OK;
+}
+
+dip_status dip_eval_host(const dip_model *M, dip_workspace *w, const void *h_records, size_t count,
+                         dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world, dip_comm *comm,
+                         dip_winner *out, void *stream) {
+    if (!M || !w || w->model != M || !out) return fail(DIP_EINVAL, "null argument");
+    if (!w->host_chunk) return fail(DIP_EINVAL, "workspace has no host staging (host_chunk = 0)");
+    if (count && !h_records) return fail(DIP_EINVAL, "null records");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t idx_bits = bits_for(std::max<uint64_t>(count, 2));
+    const bool fused = fused_ok(M, idx_bits);
+    if (!fused) return fail(DIP_ERANGE, "host path needs the fused argmin key (makespan bound too large)");
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
+    const size_t C = w->host_chunk;
+    const size_t nch = (count + C - 1) / C;
+    for (size_t c = 0; c < nch; c++) {
+        const int b = (int)(c & 1);
+        const size_t lo = c * C, cnt = std::min(C, count - lo);
+        if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(w->copy_stream, w->ev_free[b], 0));
+        CUDA_TRY(cudaMemcpyAsync(w->d_rec[b], static_cast<const uint8_t *>(h_records) + lo * M->stride,
+                                 cnt * M->stride, cudaMemcpyHostToDevice, w->copy_stream));
+        CUDA_TRY(cudaEventRecord(w->ev_copied[b], w->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(s, w->ev_copied[b], 0));
+        dip_result *dres = w->d_res + b * C;
+        dip_status st = launch_chunk(M, w, w->d_rec[b], cnt, lo, idx_bits, true, dres, nullptr, s);
+        if (st != DIP_OK) return st;
+        if (h_results) CUDA_TRY(cudaMemcpyAsync(h_results + lo, dres, cnt * sizeof(dip_result), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaEventRecord(w->ev_free[b], s));
+    }
+    w->last_results = nullptr;
+    w->last_count = count;
+    w->last_idx_bits = idx_bits;
+    w->last_fused = true;
+    return dip_argmin(M, w, count, shard_stride, rank, world, comm, out, stream);
+}
+
+// ---------------------------------------------------------------- NCCL -----------------
+dip_status dip_comm_unique_id(uint8_t id_out[128]) {
+    if (!id_out) return fail(DIP_EINVAL, "null argument");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id_out, &id, 128);
+    return DIP_OK;
+}
+
+dip_status dip_comm_init(const uint8_t id[128], int rank, int world, int cuda_device, dip_comm **out) {
+    if (!id || !out || world < 1 || rank < 0 || rank >= world) return fail(DIP_EINVAL, "bad argument");
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    dip_comm *c = new (std::nothrow) dip_comm();
+    if (!c) return fail(DIP_ENOMEM, "host allocation");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, uid, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(DIP_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    c->rank = rank;
+    c->world = world;
+    *out = c;
+    return DIP_OK;
+}
+
+dip_status dip_comm_free(dip_comm *c) {
+    if (!c) return DIP_OK;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+    return DIP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// dip_internal.h -- layout contract between the host side (dip_host.cpp) and the
+// sm_100a kernels (dip_kernels.cu). Not part of the public ABI (include/dip.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dip.h"
+
+namespace dipk {
+
+constexpr int RING_D = 8;              // depth of the smem inter-rank channels (spill beyond)
+constexpr uint64_t PEND_SHIFT = 56;    // wrap-dependency slot: pending count in bits 56..63
+constexpr uint64_t VAL_MASK = (1ull << PEND_SHIFT) - 1;
+
+// per-module constants staged in shared memory (32 B)
+struct ModInfo {
+    uint32_t K, max_split, prod_mask, cons_mask;
+    uint32_t tab_off, lay_off, nib_slot, w_max;
+};
+
+// segdec[id] bit fields: b [0,8) i [8,11) j [11,15) k [15,23) K-1 [23,31)
+__host__ __device__ inline uint32_t segdec_pack(uint32_t b, uint32_t i, uint32_t j, uint32_t k, uint32_t K) {
+    return b | (i << 8) | (j << 11) | (k << 15) | ((K - 1) << 23);
+}
+
+struct KParams {
+    // problem shape
+    uint32_t P, nmod, m, n_max, n_pad, fbw, stride;
+    uint32_t off_nib, off_fwd, off_bwd, off_fb, nsplit;   // record layout
+    // static tables, one contiguous 16-B aligned blob staged to smem by a TMA bulk copy
+    const uint8_t *blob;
+    uint32_t blob_bytes;   // multiple of 16
+    uint32_t b_modinfo, b_segdec, b_layers, b_tab, b_woff, b_wtab, b_nbi, b_sbase, b_budget;
+    // per-candidate shared-memory working set (byte offsets inside a group area)
+    uint32_t g_seqF, g_seqB, g_posF, g_posB, g_depF0, g_depBP, g_ring, g_bmf, g_bytes;
+    uint32_t warps_per_block, cpg;
+    // per launch
+    const uint8_t *records;
+    uint64_t count, index_base;
+    dip_result *results;
+    uint32_t *peaks;
+    unsigned long long *best_key;
+    unsigned long long *counter;
+    unsigned long long *spill;   // per group slot: 2 * P * n_max u64
+    uint32_t fused_key, idx_bits;
+};
+
+cudaError_t launch_eval(const KParams &kp, int G, int grid, int block, size_t smem, cudaStream_t s);
+cudaError_t prepare_eval(int G, size_t smem);
+cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm);
+cudaError_t launch_scan_argmin(const dip_result *res, uint64_t count, uint64_t index_base,
+                               unsigned long long *mk_out, unsigned long long *idx_out, cudaStream_t s);
+cudaError_t launch_scan_argmin_idx(const dip_result *res, uint64_t count, uint64_t index_base,
+                                   const unsigned long long *mk_in, unsigned long long *idx_out, cudaStream_t s);
+cudaError_t launch_make_gkey(const unsigned long long *key, unsigned long long *gkey, uint32_t idx_bits,
+                             uint32_t ibits, uint32_t rbits, uint32_t rank, cudaStream_t s);
+
+}  // namespace dipk

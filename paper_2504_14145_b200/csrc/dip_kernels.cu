@@ -1,0 +1,541 @@
+// dip_kernels.cu -- sm_100a kernels of the DIP candidate-schedule scorer.
+//
+// One persistent kernel does the whole per-candidate hot path:
+//   K1 decode      packed record -> split M_{b,i}, balanced parts (R-2), segment
+//                  orders; 128-bit coalesced loads; validation (R-11)
+//   K2 cost lookup per stage: layers(i, k*P+r) x T_i[W_j]; the tables
+//                  live in shared memory, staged once per CTA by a TMA bulk copy
+//   K3 wavefront   longest path over the stage x slot DAG (R-4..R-6), one group of
+//                  G lanes per candidate, lane = pipeline rank, lock-step rounds; per-rank
+//                  memory running sum / peak and OOM mask (R-9, R-10)
+//   K4 argmin      packed (makespan, index) key: register min -> warp shuffle -> atomicMin
+//                  (R-15)
+// Integer nanoseconds in u64; the bubble (R-16) is one IEEE double division.
+//
+// Inter-rank dependencies travel through per-rank FIFO channels in shared memory (depth
+// RING_D) with an exact spill to global memory when a producer runs more than RING_D
+// stages ahead of its consumer, so the lock-step wavefront never blocks on a full channel
+// (no false deadlocks: "no lane can progress" <=> the candidate's DAG has a cycle).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dip_internal.h"
+
+namespace dipk {
+
+// ------------------------------------------------------------------ PTX helpers ----------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ uint4 ldg128(const uint8_t *p) { return __ldg(reinterpret_cast<const uint4 *>(p)); }
+__device__ __forceinline__ uint32_t ldg32(const uint8_t *p) { return __ldg(reinterpret_cast<const uint32_t *>(p)); }
+
+template <int G>
+__device__ __forceinline__ uint64_t group_max(uint64_t v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o, G);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+template <int G>
+__device__ __forceinline__ uint64_t group_sum(uint64_t v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+    return v;
+}
+
+// ------------------------------------------------------------------ the scorer -----------
+template <int G>
+__global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(8) uint64_t blob_bar;
+    constexpr int CPG = 32 / G;
+    constexpr int D = RING_D;
+    const unsigned FULL = 0xffffffffu;
+
+    // (a1) static tables -> smem, one TMA bulk copy per CTA
+    if (threadIdx.x == 0) {
+        mbar_init(&blob_bar, 1);
+        mbar_expect_tx(&blob_bar, kp.blob_bytes);
+        tma_bulk_g2s(smem, kp.blob, kp.blob_bytes, &blob_bar);
+    }
+    __syncthreads();
+    mbar_wait(&blob_bar, 0);
+
+    const ModInfo *mi = reinterpret_cast<const ModInfo *>(smem + kp.b_modinfo);
+    const uint32_t *segdec = reinterpret_cast<const uint32_t *>(smem + kp.b_segdec);
+    const uint16_t *layers = reinterpret_cast<const uint16_t *>(smem + kp.b_layers);
+    const uint4 *tab = reinterpret_cast<const uint4 *>(smem + kp.b_tab);
+    const uint32_t *woff = reinterpret_cast<const uint32_t *>(smem + kp.b_woff);
+    const uint16_t *wtab = reinterpret_cast<const uint16_t *>(smem + kp.b_wtab);
+    const uint16_t *nbi = reinterpret_cast<const uint16_t *>(smem + kp.b_nbi);
+    const uint16_t *sbase = reinterpret_cast<const uint16_t *>(smem + kp.b_sbase);
+    const uint32_t *budget = reinterpret_cast<const uint32_t *>(smem + kp.b_budget);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane / G, r = lane % G;
+    const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
+    const uint32_t P = kp.P, nmod = kp.nmod, nq = kp.m * kp.nmod, n_max = kp.n_max;
+    uint8_t *ga = smem + kp.blob_bytes + (size_t)(warp * CPG + g) * kp.g_bytes;
+    uint16_t *seqF = reinterpret_cast<uint16_t *>(ga + kp.g_seqF);
+    uint16_t *seqB = reinterpret_cast<uint16_t *>(ga + kp.g_seqB);
+    uint32_t *posF = reinterpret_cast<uint32_t *>(ga + kp.g_posF);
+    uint32_t *posB = reinterpret_cast<uint32_t *>(ga + kp.g_posB);
+    uint64_t *depF0 = reinterpret_cast<uint64_t *>(ga + kp.g_depF0);
+    uint64_t *depBP = reinterpret_cast<uint64_t *>(ga + kp.g_depBP);
+    uint64_t *ringF = reinterpret_cast<uint64_t *>(ga + kp.g_ring);
+    uint64_t *ringB = ringF + P * D;
+    uint32_t *segInfo = reinterpret_cast<uint32_t *>(ga + kp.g_ring);   // alias: decode only
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(ga + kp.g_depBP);   // alias: validation only
+    uint8_t *Mb = ga + kp.g_bmf;          // M_{b,i}
+    uint8_t *Pc = Mb + nq;                // present producer sub-microbatches of (b,i)
+    uint8_t *Cc = Pc + nq;                // present consumer sub-microbatches of (b,i)
+    const uint64_t slot_id = ((uint64_t)blockIdx.x * kp.warps_per_block + warp) * CPG + g;
+    unsigned long long *spF = kp.spill + slot_id * 2ull * P * n_max;
+    unsigned long long *spB = spF + (size_t)P * n_max;
+    const uint32_t nwords = (n_max + 31) / 32;
+
+    unsigned long long best = ~0ull;
+
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(kp.counter, (unsigned long long)CPG);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= kp.count) break;
+        const uint64_t cand = base + g;
+        const bool gvalid = cand < kp.count;
+        const uint8_t *rec = kp.records + (gvalid ? cand : 0) * (uint64_t)kp.stride;
+
+        // ---------------- K1: decode + validate ----------------
+        const uint32_t hdr = ldg32(rec);
+        const uint32_t n = hdr & 0xFFFFu;
+        bool bad = !gvalid || (hdr >> 16) != 0 || n > n_max;
+        uint32_t nsum = 0;
+        for (uint32_t q = r; q < nq; q += G) {
+            const uint32_t b = q / nmod, i = q - b * nmod;
+            const uint32_t N = nbi[q], Mx = mi[i].max_split;
+            uint32_t M;
+            if (Mx > 1) {
+                const uint32_t nib = b * kp.nsplit + mi[i].nib_slot;
+                M = (__ldg(rec + kp.off_nib + (nib >> 1)) >> ((nib & 1) * 4)) & 15u;
+            } else {
+                M = N > 0 ? 1u : 0u;
+            }
+            const uint32_t hi = N < Mx ? N : Mx;
+            if ((N == 0) != (M == 0) || M > hi) bad = true;
+            Mb[q] = (uint8_t)(M > 15 ? 15 : M);
+            nsum += M * mi[i].K;
+        }
+        nsum = (uint32_t)group_sum<G>(nsum);
+        if (nsum != n) bad = true;
+        for (uint32_t w = r; w < 2 * nwords; w += G) bitmap[w] = 0;
+        __syncwarp();
+        for (uint32_t q = r; q < nq; q += G) {   // join fan-in / fan-out counts (R-5, R-6)
+            const uint32_t b = q / nmod, i = q - b * nmod;
+            uint32_t pc = 0, cc = 0;
+            for (uint32_t x = 0; x < nmod; x++) {
+                if ((mi[i].prod_mask >> x) & 1u) pc += Mb[b * nmod + x];
+                if ((mi[i].cons_mask >> x) & 1u) cc += Mb[b * nmod + x];
+            }
+            Pc[q] = (uint8_t)pc;
+            Cc[q] = (uint8_t)cc;
+        }
+        // sequences: 16-byte loads, copy to smem, check they are permutations of the present ids
+        const uint32_t nv = kp.n_pad / 8;
+        for (uint32_t v = r; v < nv; v += G) {
+            const uint4 f4 = ldg128(rec + kp.off_fwd + 16 * v);
+            const uint4 b4 = ldg128(rec + kp.off_bwd + 16 * v);
+            reinterpret_cast<uint4 *>(seqF)[v] = f4;
+            reinterpret_cast<uint4 *>(seqB)[v] = b4;
+            const uint32_t fw[4] = {f4.x, f4.y, f4.z, f4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const uint32_t pos = 8 * v + e;
+                const uint32_t idf = (fw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                const uint32_t idb = (bw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                if (pos < n) {
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const uint32_t id = h ? idb : idf;
+                        if (id >= n_max) { bad = true; continue; }
+                        const uint32_t dc = segdec[id];
+                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15;
+                        if (j >= Mb[b * nmod + i]) { bad = true; continue; }
+                        const uint32_t old = atomicOr(&bitmap[h * nwords + (id >> 5)], 1u << (id & 31));
+                        if (old & (1u << (id & 31))) bad = true;
+                    }
+                } else if (idf != 0xFFFFu || idb != 0xFFFFu) {
+                    bad = true;
+                }
+            }
+        }
+        // F/B bit rows: exactly n ones in [0, 2n), zeros beyond
+        uint32_t wcur = 0, wnext = 0;
+        if (r < (int)P) {
+            const uint32_t lim = 2 * n;
+            uint32_t ones = 0;
+            for (uint32_t w = 0; w < kp.fbw; w++) {
+                const uint32_t word = ldg32(rec + kp.off_fb + 4 * (w * P + r));
+                if (w == 0) wcur = word;
+                if (w == 1) wnext = word;
+                if (32 * w + 32 <= lim) {
+                    ones += __popc(word);
+                } else if (32 * w >= lim) {
+                    if (word) bad = true;
+                } else {
+                    const uint32_t msk = (1u << (lim - 32 * w)) - 1u;
+                    ones += __popc(word & msk);
+                    if (word & ~msk) bad = true;
+                }
+            }
+            if (ones != n) bad = true;
+        }
+        bad = (__ballot_sync(FULL, bad) & gmask) != 0;
+
+        // ---------------- K2: per-segment cost rows + wrap-dependency init ----------------
+        __syncwarp();
+        if (!bad) {
+            for (uint32_t s = r; s < n_max; s += G) {
+                const uint32_t dc = segdec[s];
+                const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
+                const uint32_t Km1 = dc >> 23, q = b * nmod + i, M = Mb[q];
+                uint64_t f0 = 0, bp = 0;
+                if (j < M) {
+                    const uint32_t W = wtab[woff[q] + M * (M - 1) / 2 + j];
+                    segInfo[s] = (mi[i].tab_off + W) | ((mi[i].lay_off + k * P) << 16);
+                    if (k > 0) f0 = 1ull << PEND_SHIFT;
+                    else if (j == 0) f0 = (uint64_t)Pc[q] << PEND_SHIFT;
+                    if (k < Km1) bp = 1ull << PEND_SHIFT;
+                    else if (Cc[q] == 0) bp = 1ull << PEND_SHIFT;            // loss turnaround (R-6)
+                    else if (j == 0) bp = (uint64_t)Cc[q] << PEND_SHIFT;     // consumer join (R-5)
+                }
+                depF0[s] = f0;
+                depBP[s] = bp;
+            }
+        }
+        __syncwarp();
+        if (!bad) {
+            for (uint32_t p = r; p < n; p += G) {
+                posF[p] = segInfo[seqF[p]];
+                posB[p] = segInfo[seqB[p]];
+            }
+        }
+        __syncwarp();
+
+        // ---------------- K3: lock-step wavefront longest path ----------------
+        const uint32_t S2 = 2 * n;
+        bool done = bad || r >= (int)P || n == 0;
+        bool dl = false;
+        uint32_t t = 0, fi = 0, bi = 0;
+        uint64_t tlast = 0, busy = 0;
+        uint32_t cur = 0, peak = 0;
+        for (;;) {
+            const uint32_t packed = fi | (bi << 16);
+            const uint32_t up = __shfl_up_sync(FULL, packed, 1, G);
+            const uint32_t dn = __shfl_down_sync(FULL, packed, 1, G);
+            bool ready = false, isB = false;
+            uint64_t dep = 0;
+            uint32_t pos = 0, s = 0, dc = 0;
+            bool addp = false;
+            if (!done) {
+                isB = (wcur >> (t & 31)) & 1u;
+                if (!isB) {
+                    pos = posF[fi];
+                    if (r == 0) {                      // wrap / join edge from rank P-1 (R-4, R-5)
+                        s = seqF[fi];
+                        dc = segdec[s];
+                        const uint32_t j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF, K = (dc >> 23) + 1;
+                        const uint64_t v = depF0[k ? s : s - j * K];
+                        ready = (v >> PEND_SHIFT) == 0;
+                        dep = v & VAL_MASK;
+                    } else {                           // F(s, r-1) -> F(s, r)
+                        const uint32_t pf = up & 0xFFFFu;
+                        ready = pf > fi;
+                        if (ready) {
+                            dep = (fi + D >= pf) ? ringF[(r - 1) * D + (fi % D)] : spF[(r - 1) * n_max + fi];
+                            addp = true;
+                        }
+                    }
+                } else {
+                    pos = posB[bi];
+                    if (r == (int)P - 1) {             // wrap / join / turnaround edge from rank 0
+                        s = seqB[bi];
+                        dc = segdec[s];
+                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15;
+                        const uint32_t k = (dc >> 15) & 0xFF, Km1 = dc >> 23;
+                        uint32_t slot = s;
+                        addp = true;
+                        if (k == Km1) {
+                            if (Cc[b * nmod + i] == 0) addp = false;      // turnaround: same rank
+                            else slot = s - j * (Km1 + 1);                  // join slot id(b,i,0,K-1)
+                        }
+                        const uint64_t v = depBP[slot];
+                        ready = (v >> PEND_SHIFT) == 0;
+                        dep = v & VAL_MASK;
+                    } else {                           // B(s, r+1) -> B(s, r)
+                        const uint32_t pb = dn >> 16;
+                        ready = pb > bi;
+                        if (ready) {
+                            dep = (bi + D >= pb) ? ringB[(r + 1) * D + (bi % D)] : spB[(r + 1) * n_max + bi];
+                            addp = true;
+                        }
+                    }
+                }
+            }
+            const uint32_t prog = __ballot_sync(FULL, ready);
+            const uint32_t alive = __ballot_sync(FULL, !done);
+            if (alive == 0) break;
+            if ((alive & gmask) && !(prog & gmask)) {   // no lane of this group can move: a cycle
+                dl = true;
+                done = true;
+            }
+            __syncwarp();
+            if (ready) {
+                const uint4 T = tab[pos & 0xFFFFu];
+                const uint64_t lay = layers[(pos >> 16) + r];
+                const uint64_t lat = lay * (uint64_t)(isB ? T.y : T.x);
+                if (addp) dep += T.w;
+                const uint64_t st = dep > tlast ? dep : tlast;
+                const uint64_t end = st + lat;
+                tlast = end;
+                busy += lat;
+                const uint32_t a = (uint32_t)lay * T.z;
+                if (!isB) {
+                    cur += a;
+                    peak = cur > peak ? cur : peak;
+                    if (r == (int)P - 1) {             // publish to rank 0 / the loss turnaround
+                        s = seqF[fi];
+                        dc = segdec[s];
+                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
+                        const uint32_t k = (dc >> 15) & 0xFF, Km1 = dc >> 23;
+                        const uint64_t v = end + T.w;
+                        if (k < Km1) {
+                            depF0[s + 1] = v;
+                        } else {
+                            const uint32_t cm = mi[i].cons_mask;
+                            bool any = false;
+                            for (uint32_t c = 0; c < nmod; c++) {
+                                if (!((cm >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                                uint64_t *sl = &depF0[sbase[b * nmod + c]];
+                                const uint64_t old = *sl;
+                                const uint64_t ov = old & VAL_MASK;
+                                *sl = (v > ov ? v : ov) | (((old >> PEND_SHIFT) - 1) << PEND_SHIFT);
+                                any = true;
+                            }
+                            if (!any) depBP[s] = end;
+                        }
+                    } else {                           // channel to rank r+1 (exact spill)
+                        const uint32_t nf = dn & 0xFFFFu;
+                        uint64_t *slot = &ringF[r * D + (fi % D)];
+                        if (fi >= D && nf + D <= fi) spF[r * n_max + fi - D] = *slot;
+                        *slot = end;
+                    }
+                    fi++;
+                } else {
+                    cur -= a;
+                    if (r == 0) {                      // publish to rank P-1
+                        s = seqB[bi];
+                        dc = segdec[s];
+                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, k = (dc >> 15) & 0xFF;
+                        if (k > 0) {
+                            depBP[s - 1] = end;
+                        } else {
+                            const uint32_t pm = mi[i].prod_mask;
+                            for (uint32_t p = 0; p < nmod; p++) {
+                                if (!((pm >> p) & 1u) || Mb[b * nmod + p] == 0) continue;
+                                uint64_t *sl = &depBP[sbase[b * nmod + p] + mi[p].K - 1];
+                                const uint64_t old = *sl;
+                                const uint64_t ov = old & VAL_MASK;
+                                *sl = (end > ov ? end : ov) | (((old >> PEND_SHIFT) - 1) << PEND_SHIFT);
+                            }
+                        }
+                    } else {                           // channel to rank r-1
+                        const uint32_t nb = up >> 16;
+                        uint64_t *slot = &ringB[r * D + (bi % D)];
+                        if (bi >= D && nb + D <= bi) spB[r * n_max + bi - D] = *slot;
+                        *slot = end;
+                    }
+                    bi++;
+                }
+                t++;
+                if ((t & 31) == 0 && t < S2) {
+                    wcur = wnext;
+                    const uint32_t nw = (t >> 5) + 1;
+                    if (nw < kp.fbw) wnext = ldg32(rec + kp.off_fb + 4 * (nw * P + r));
+                }
+                if (t == S2) done = true;
+            }
+            __syncwarp();
+        }
+        // deadlocked candidates: finish the order-only memory scan (R-9)
+        if (dl && r < (int)P) {
+            while (t < S2) {
+                if ((t & 31) == 0 && t > 0) wcur = ldg32(rec + kp.off_fb + 4 * ((t >> 5) * P + r));
+                const bool b1 = (wcur >> (t & 31)) & 1u;
+                const uint32_t ps = b1 ? posB[bi++] : posF[fi++];
+                const uint32_t a = (uint32_t)layers[(ps >> 16) + r] * tab[ps & 0xFFFFu].z;
+                if (!b1) { cur += a; peak = cur > peak ? cur : peak; }
+                else cur -= a;
+                t++;
+            }
+        }
+
+        // ---------------- results + K4 argmin ----------------
+        const uint64_t mk = group_max<G>(tlast);
+        const uint64_t bsum = group_sum<G>(busy);
+        const bool over = r < (int)P && !bad && peak > budget[r < (int)P ? r : 0];
+        const uint32_t oom = (__ballot_sync(FULL, over) & gmask) >> (g * G);
+        if (gvalid) {
+            uint32_t status;
+            uint64_t mko;
+            double bub;
+            if (bad) { status = DIP_CAND_BAD_ENCODING; mko = ~0ull; bub = -1.0; }
+            else if (dl) { status = DIP_CAND_DEADLOCK; mko = ~0ull; bub = -1.0; }
+            else {
+                status = oom ? DIP_CAND_OOM : DIP_CAND_OK;
+                mko = mk;
+                const uint64_t den = (uint64_t)P * mk;
+                bub = den ? (double)(den - bsum) / (double)den : 0.0;
+            }
+            if (r == 0) {
+                dip_result res;
+                res.makespan_ns = mko;
+                res.status = status;
+                res.oom_mask = bad ? 0u : oom;
+                res.bubble = bub;
+                kp.results[cand] = res;
+                if (status == DIP_CAND_OK && kp.fused_key) {
+                    const unsigned long long key = ((unsigned long long)mk << kp.idx_bits) | (kp.index_base + cand);
+                    best = key < best ? key : best;
+                }
+            }
+            if (kp.peaks && r < (int)P) kp.peaks[cand * P + r] = bad ? 0u : peak;
+        }
+        __syncwarp();
+    }
+    // fused argmin epilogue: warp shuffle min, one atomicMin per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(FULL, best, o);
+        best = w < best ? w : best;
+    }
+    if (lane == 0 && best != ~0ull) atomicMin(kp.best_key, best);
+}
+
+// exact fallback argmin when the packed key could overflow: pass 1 min makespan
+__global__ void scan_min_makespan(const dip_result *res, uint64_t count, unsigned long long *mk_out) {
+    unsigned long long best = ~0ull;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < count; x += (uint64_t)gridDim.x * blockDim.x)
+        if (res[x].status == DIP_CAND_OK && res[x].makespan_ns < best) best = res[x].makespan_ns;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, best, o);
+        best = w < best ? w : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(mk_out, best);
+}
+// pass 2: min index among candidates with that makespan
+__global__ void scan_min_index(const dip_result *res, uint64_t count, uint64_t index_base,
+                               const unsigned long long *mk_in, unsigned long long *idx_out) {
+    const unsigned long long target = *mk_in;
+    unsigned long long best = ~0ull;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < count; x += (uint64_t)gridDim.x * blockDim.x)
+        if (res[x].status == DIP_CAND_OK && res[x].makespan_ns == target && index_base + x < best) best = index_base + x;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, best, o);
+        best = w < best ? w : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(idx_out, best);
+}
+// per-GPU key (makespan << idx_bits | local) -> cross-rank key (makespan, rank, local)
+__global__ void make_gkey(const unsigned long long *key, unsigned long long *gkey, uint32_t idx_bits, uint32_t ibits,
+                          uint32_t rbits, uint32_t rank) {
+    const unsigned long long k = *key;
+    if (k == ~0ull) { *gkey = ~0ull; return; }
+    const unsigned long long mk = k >> idx_bits, local = k & ((1ull << idx_bits) - 1);
+    *gkey = (mk << (rbits + ibits)) | ((unsigned long long)rank << ibits) | local;
+}
+
+template <int G>
+static cudaError_t launch_g(const KParams &kp, int grid, int block, size_t smem, cudaStream_t s) {
+    dip_eval_kernel<G><<<grid, block, smem, s>>>(kp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval(const KParams &kp, int G, int grid, int block, size_t smem, cudaStream_t s) {
+    switch (G) {
+    case 4: return launch_g<4>(kp, grid, block, smem, s);
+    case 8: return launch_g<8>(kp, grid, block, smem, s);
+    case 16: return launch_g<16>(kp, grid, block, smem, s);
+    case 32: return launch_g<32>(kp, grid, block, smem, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int G>
+static const void *kfun() { return reinterpret_cast<const void *>(&dip_eval_kernel<G>); }
+static const void *kernel_for(int G) {
+    switch (G) {
+    case 4: return kfun<4>();
+    case 8: return kfun<8>();
+    case 16: return kfun<16>();
+    case 32: return kfun<32>();
+    default: return nullptr;
+    }
+}
+
+cudaError_t prepare_eval(int G, size_t smem) {
+    const void *f = kernel_for(G);
+    if (!f) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm) {
+    const void *f = kernel_for(G);
+    if (!f) return cudaErrorInvalidValue;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+}
+
+cudaError_t launch_scan_argmin(const dip_result *res, uint64_t count, uint64_t /*index_base*/,
+                               unsigned long long *mk_out, unsigned long long * /*idx_out*/, cudaStream_t s) {
+    scan_min_makespan<<<592, 256, 0, s>>>(res, count, mk_out);
+    return cudaGetLastError();
+}
+cudaError_t launch_scan_argmin_idx(const dip_result *res, uint64_t count, uint64_t index_base,
+                                   const unsigned long long *mk_in, unsigned long long *idx_out, cudaStream_t s) {
+    scan_min_index<<<592, 256, 0, s>>>(res, count, index_base, mk_in, idx_out);
+    return cudaGetLastError();
+}
+cudaError_t launch_make_gkey(const unsigned long long *key, unsigned long long *gkey, uint32_t idx_bits,
+                             uint32_t ibits, uint32_t rbits, uint32_t rank, cudaStream_t s) {
+    make_gkey<<<1, 1, 0, s>>>(key, gkey, idx_bits, ibits, rbits, rank);
+    return cudaGetLastError();
+}
+
+}  // namespace dipk

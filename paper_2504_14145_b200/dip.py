@@ -1,0 +1,272 @@
+"""Thin ctypes binding of libdip.so (include/dip.h). Argument marshalling only:
+every step of the scoring path runs in the library's sm_100a kernels.
+
+PyTorch is used by callers for device memory, streams and process groups; this
+module takes raw pointers (tensor.data_ptr()) or numpy arrays, and fails loudly
+if the compiled library is missing -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdip.so")
+
+DIP_OK = 0
+CAND_OK, CAND_OOM, CAND_DEADLOCK, CAND_BAD = 0, 1, 2, 3
+
+RESULT_DTYPE = np.dtype([("makespan_ns", "<u8"), ("status", "<u4"), ("oom_mask", "<u4"), ("bubble", "<f8")])
+assert RESULT_DTYPE.itemsize == 24
+
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+
+class _ModuleDesc(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_uint32), ("K", ctypes.c_uint32), ("max_split", ctypes.c_uint32),
+                ("w_max", ctypes.c_uint32), ("producer_mask", ctypes.c_uint32),
+                ("chunk_layers", ctypes.c_void_p), ("f_ns", ctypes.c_void_p), ("b_ns", ctypes.c_void_p),
+                ("act_kib", ctypes.c_void_p), ("p2p_ns", ctypes.c_void_p)]
+
+
+class _ProblemDesc(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_uint32), ("n_modules", ctypes.c_uint32), ("m", ctypes.c_uint32),
+                ("modules", ctypes.POINTER(_ModuleDesc)), ("inst_off", ctypes.c_void_p),
+                ("inst_units", ctypes.c_void_p), ("budget_kib", ctypes.c_void_p)]
+
+
+class _ModelInfo(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("P", "n_modules", "m", "n_max", "fbw", "record_stride",
+                                                "group_lanes", "smem_per_block", "warps_per_block",
+                                                "blocks_per_sm", "grid")] + [("makespan_bound", ctypes.c_uint64)]
+
+
+class _CandBatch(ctypes.Structure):
+    _fields_ = [("split", ctypes.c_void_p), ("n", ctypes.c_void_p), ("fwd_seq", ctypes.c_void_p),
+                ("bwd_seq", ctypes.c_void_p), ("fb_bits", ctypes.c_void_p)]
+
+
+class _Winner(ctypes.Structure):
+    _fields_ = [("found", ctypes.c_int32), ("rank", ctypes.c_int32), ("global_index", ctypes.c_uint64),
+                ("makespan_ns", ctypes.c_uint64)]
+
+
+@dataclass
+class Winner:
+    found: bool
+    rank: int
+    global_index: int
+    makespan_ns: int
+
+
+_lib = None
+
+
+def lib():
+    """Load libdip.so (built in-tree by paper_2504_14145_b200/build.py); raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python paper_2504_14145_b200/build.py` "
+                           "(there is no CPU fallback for the scoring path)")
+    L = ctypes.CDLL(LIB_PATH)
+    st = ctypes.c_int
+    vp = ctypes.c_void_p
+    L.dip_load_cost_model.argtypes = [ctypes.POINTER(_ProblemDesc), ctypes.c_int, ctypes.POINTER(vp)]
+    L.dip_model_free.argtypes = [vp]
+    L.dip_model_get_info.argtypes = [vp, ctypes.POINTER(_ModelInfo)]
+    L.dip_encode_candidates.argtypes = [vp, ctypes.POINTER(_CandBatch), ctypes.c_size_t, vp, ctypes.c_int]
+    L.dip_workspace_create.argtypes = [vp, ctypes.c_size_t, ctypes.POINTER(vp)]
+    L.dip_workspace_free.argtypes = [vp]
+    L.dip_eval_schedules.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
+    L.dip_argmin.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp,
+                             ctypes.POINTER(_Winner), vp]
+    L.dip_eval_host.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                vp, ctypes.POINTER(_Winner), vp]
+    L.dip_comm_unique_id.argtypes = [vp]
+    L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    L.dip_comm_free.argtypes = [vp]
+    for f in ("dip_load_cost_model", "dip_model_free", "dip_model_get_info", "dip_encode_candidates",
+              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_argmin", "dip_eval_host",
+              "dip_comm_unique_id", "dip_comm_init", "dip_comm_free"):
+        getattr(L, f).restype = st
+    L.dip_launch_count.restype = ctypes.c_uint64
+    L.dip_launch_count.argtypes = []
+    L.dip_status_str.restype = ctypes.c_char_p
+    L.dip_status_str.argtypes = [st]
+    L.dip_last_error.restype = ctypes.c_char_p
+    L.dip_last_error.argtypes = []
+    _lib = L
+    return L
+
+
+class DipError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        L = lib()
+        super().__init__(f"{where}: {L.dip_status_str(code).decode()} ({L.dip_last_error().decode()})")
+        self.code = code
+
+
+def _check(code: int, where: str):
+    if code != DIP_OK:
+        raise DipError(code, where)
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return 0
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return 0
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def launch_count() -> int:
+    return int(lib().dip_launch_count())
+
+
+class Model:
+    """dip_load_cost_model over a problem-like object (attributes P, m, modules[...] with
+    L, K, max_split, w_max, producer_mask, f_ns, b_ns, act_kib, p2p_ns, chunk_layers;
+    inst_off, inst_units, budget_kib)."""
+
+    def __init__(self, pb, device: int = 0):
+        L = lib()
+        keep = []
+
+        def arr(a, dt):
+            x = np.ascontiguousarray(a, dt)
+            keep.append(x)
+            return x.ctypes.data
+
+        mods = (_ModuleDesc * len(pb.modules))()
+        for i, md in enumerate(pb.modules):
+            mods[i] = _ModuleDesc(md.L, md.K, md.max_split, md.w_max, md.producer_mask,
+                                  arr(md.chunk_layers, np.uint32) if md.chunk_layers is not None else None,
+                                  arr(md.f_ns, np.uint32), arr(md.b_ns, np.uint32), arr(md.act_kib, np.uint32),
+                                  arr(md.p2p_ns, np.uint32))
+        units = np.ascontiguousarray(pb.inst_units, np.uint16)
+        if units.size == 0:
+            units = np.zeros(1, np.uint16)
+        keep.append(units)
+        d = _ProblemDesc(pb.P, len(pb.modules), pb.m, mods, arr(pb.inst_off, np.uint32), units.ctypes.data,
+                         arr(pb.budget_kib, np.uint32))
+        h = ctypes.c_void_p()
+        _check(L.dip_load_cost_model(ctypes.byref(d), device, ctypes.byref(h)), "dip_load_cost_model")
+        self.handle = h
+        self.device = device
+        inf = _ModelInfo()
+        _check(L.dip_model_get_info(h, ctypes.byref(inf)), "dip_model_get_info")
+        self.info = {k: getattr(inf, k) for k, _ in _ModelInfo._fields_}
+        self.P = inf.P
+        self.n_max = inf.n_max
+        self.fbw = inf.fbw
+        self.stride = inf.record_stride
+
+    def encode(self, cands, out=None, threads: int = 0):
+        """Pack host-view candidates (split, n, fwd, bwd, fb arrays) into records; returns `out`
+        (a numpy uint8 array, or the given numpy array / pinned torch tensor)."""
+        count = len(cands.n)
+        if out is None:
+            out = np.zeros(count * self.stride, np.uint8)
+        arrs = [np.ascontiguousarray(getattr(cands, k)) for k in ("split", "n", "fwd", "bwd", "fb")]
+        assert arrs[0].dtype == np.uint8 and arrs[1].dtype == np.uint32 and arrs[2].dtype == np.uint16
+        assert arrs[4].dtype == np.uint32
+        cb = _CandBatch(*[a.ctypes.data for a in arrs])
+        _check(lib().dip_encode_candidates(self.handle, ctypes.byref(cb), count, _ptr(out), threads),
+               "dip_encode_candidates")
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dip_model_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Workspace:
+    def __init__(self, model: Model, host_chunk: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().dip_workspace_create(model.handle, host_chunk, ctypes.byref(h)), "dip_workspace_create")
+        self.handle = h
+        self.model = model
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dip_workspace_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Comm:
+    """NCCL communicator owned by libdip (bootstrapped through torch.distributed)."""
+
+    def __init__(self, uid: bytes, rank: int, world: int, device: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        _check(lib().dip_comm_init(buf, rank, world, device, ctypes.byref(h)), "dip_comm_init")
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().dip_comm_unique_id(buf), "dip_comm_unique_id")
+        return bytes(buf)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dip_comm_free(self.handle)
+            self.handle = None
+
+
+def eval_schedules(model: Model, ws: Workspace, d_records, count: int, d_results, d_peaks=None, stream=None):
+    _check(lib().dip_eval_schedules(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results),
+                                    _ptr(d_peaks), _stream(stream)), "dip_eval_schedules")
+
+
+def argmin(model: Model, ws: Workspace, count: int, shard_stride: Optional[int] = None, rank: int = 0,
+           world: int = 1, comm: Optional[Comm] = None, stream=None) -> Winner:
+    w = _Winner()
+    _check(lib().dip_argmin(model.handle, ws.handle, count, shard_stride if shard_stride is not None else count,
+                            rank, world, comm.handle if comm else None, ctypes.byref(w), _stream(stream)),
+           "dip_argmin")
+    return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
+
+
+def eval_host(model: Model, ws: Workspace, h_records, count: int, h_results=None, shard_stride: Optional[int] = None,
+              rank: int = 0, world: int = 1, comm: Optional[Comm] = None, stream=None) -> Winner:
+    w = _Winner()
+    _check(lib().dip_eval_host(model.handle, ws.handle, _ptr(h_records), count, _ptr(h_results),
+                               shard_stride if shard_stride is not None else count, rank, world,
+                               comm.handle if comm else None, ctypes.byref(w), _stream(stream)), "dip_eval_host")
+    return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
+
+
+def results_view(host_bytes) -> np.ndarray:
+    """View a host copy of dip_result[count] (uint8 bytes) as a structured numpy array."""
+    a = np.asarray(host_bytes)
+    return a.view(RESULT_DTYPE)
