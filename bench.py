@@ -1,0 +1,317 @@
+#!/usr/bin/env python3
+"""Benchmark: candidate schedules evaluated per second on 1/2/4/8 B200s (BASELINE.json metric).
+
+One step = one pass of the whole hot path over this GPU's shard of one input batch's
+candidates: decode + cost lookup + longest-path DP + memory peaks/OOM + bubble + fused
+argmin (dip_eval_schedules), then dip_argmin (one NCCL allreduce of the packed key at N>1).
+Weak scaling: every GPU scores its own contiguous shard of `--per-gpu` candidates
+(94B config: 1,048,576 per GPU = the 8M-candidate config at 8 GPUs).
+
+  python bench.py [--gpus N --steps K --warmup W --config 94B]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+  python bench.py --impl reference ...   (the CPU oracle on the host cores, rank 0 only)
+
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+METRIC = "candidate schedules evaluated/sec"
+UNIT = "candidates/s"
+DEFAULT_PER_GPU = {"toy": 256, "12B": 65536, "37B": 1 << 20, "T2V": 1 << 20, "94B": 1 << 20}
+CONFIG_DESC = {
+    "toy": "toy: P=4, ViT+LLM, m=4",
+    "12B": "12B VLM (ViT-5B + Llama3-8B): P=8, m=16, K_LLM=4",
+    "37B": "37B VLM (ViT-5B + Qwen2-32B): P=8 x K_LLM=2 (16 virtual stages), m=32",
+    "T2V": "T2V LMM (Qwen2-32B text-enc + VAE + DiT-30B): P=16, m=32",
+    "94B": "94B LMM (ViT-22B + Qwen2-72B): P=32, m=64, K_LLM=2",
+}
+INT_OPS_PER_STAGE = 10          # algorithmic int32-equivalent ops per stage node
+INT_OPS_PER_CLK_SM = 128        # 4 SMSP x 1 warp-instr/clk (ALU + FMA pipes, B300_MICROARCH.md)
+FALLBACK_HBM_GBS = 6650.0       # B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", FALLBACK_HBM_GBS), d.get("sm_max_mhz", 1965.0), "measured"
+    return FALLBACK_HBM_GBS, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            self.p.wait()
+        self.f.flush()
+
+    def summary(self):
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nme)
+        os.unlink(self.f.name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(pb, cs, sample: int, threads: int, core_seconds: float = 20.0):
+    """The oracle, as it stands, on all host cores over a bounded sample (~20 core-s of work)."""
+    import oracle
+    probe = cs.subset(np.arange(min(256, cs.count)))
+    t0 = time.perf_counter()
+    oracle.evaluate(pb, probe, threads=threads)
+    per_cand = (time.perf_counter() - t0) * threads / max(1, probe.count)
+    if sample <= 0:
+        sample = int(min(cs.count, max(1024, core_seconds / max(per_cand, 1e-7))))
+    sub = cs.subset(np.arange(min(sample, cs.count)))
+    t0 = time.perf_counter()
+    oracle.evaluate(pb, sub, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": sub.count / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {sub.count} candidates of rank 0's shard ({dt:.1f} s wall, "
+                      f"{dt * threads:.0f} core-s)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle, as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    pb = gen.make_problem(args.config)
+    threads = os.cpu_count() or 1
+    per = args.ref_sample
+    cs = gen.generate(pb, 0, per * (args.warmup + args.steps), threads=threads)
+    times = []
+    for s in range(args.warmup + args.steps):
+        sub = cs.subset(np.arange(s * per, (s + 1) * per))
+        t0 = time.perf_counter()
+        oracle.evaluate(pb, sub, threads=threads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = per * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": dict(config_block(args, pb, args.per_gpu or DEFAULT_PER_GPU[args.config], world),
+                           reference_sample_per_step=per),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{per} candidates per step (a bounded sample of the workload)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, pb, per_gpu, world):
+    return {"workload": f"{args.config} -- {CONFIG_DESC[args.config]}", "candidates_per_gpu": per_gpu,
+            "total_candidates": per_gpu * world, "P": pb.P, "m": pb.m, "n_max": pb.n_max,
+            "parallelism": f"candidate-dp{world}", "seed": pb.seed,
+            "l2": "no flush: records > 126 MB L2 per step" if per_gpu * 1000 > (256 << 20) else
+                  "L2 flushed (512 MB write) between timed steps, outside the step events"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dip", choices=["dip", "reference"])
+    ap.add_argument("--config", default="94B", choices=gen.CONFIG_NAMES)
+    ap.add_argument("--per-gpu", type=int, default=0)
+    ap.add_argument("--ref-sample", type=int, default=4096)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="0: ~20 core-seconds of oracle work")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--host-chunk", type=int, default=65536)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_14145_b200 as dip
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pb = gen.make_problem(args.config)
+    per = args.per_gpu or DEFAULT_PER_GPU[args.config]
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    gthreads = max(1, (os.cpu_count() or 1) // local_world)
+    t0 = time.time()
+    cs = gen.generate(pb, rank * per, per, threads=gthreads)      # contiguous rank-major shard
+    t_gen = time.time() - t0
+    model = dip.Model(pb, local)
+    ws = dip.Workspace(model, host_chunk=0 if args.no_e2e else args.host_chunk)
+    h_rec = torch.empty(per * model.stride, dtype=torch.uint8).pin_memory()
+    model.encode(cs, out=h_rec, threads=gthreads)
+    d_rec = h_rec.to(dev)
+    d_res = torch.empty(per * 24, dtype=torch.uint8, device=dev)
+    d_pk = torch.empty((per, pb.P), dtype=torch.int32, device=dev)
+    comm = None
+    if world > 1:
+        obj = [dip.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = dip.Comm(obj[0], rank, world, local)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dip.eval_schedules(model, ws, d_rec, per, d_res, d_pk, stream=stream)
+        return dip.argmin(model, ws, per, per, rank, world, comm, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        win = step()
+    res = dip.results_view(d_res.cpu().numpy())
+    hist = np.bincount(res["status"], minlength=4).tolist()
+    stages = int(np.sum(np.where(res["status"] != 3, 2 * cs.n.astype(np.int64) * pb.P, 0)))
+
+    # ---- timed region: device-resident inputs
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    # inputs smaller than L2 (126 MB): flush it between timed steps by writing a 512 MB buffer,
+    # outside the per-step events; larger inputs need no flush
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if per * model.stride < (256 << 20) else None
+    s0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    s1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = dip.launch_count()
+    with ClockSampler() as clk:
+        for s in range(args.steps):
+            if flush is not None:
+                flush.fill_(s & 0xFF)
+            s0[s].record(stream)
+            dip.eval_schedules(model, ws, d_rec, per, d_res, d_pk, stream=stream)
+            k1[s].record(stream)
+            win = dip.argmin(model, ws, per, per, rank, world, comm, stream=stream)
+            s1[s].record(stream)
+        torch.cuda.synchronize()
+    launches = dip.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    t_ms = sum(a.elapsed_time(b) for a, b in zip(s0, s1))
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(s0, k1))
+    tt = torch.tensor([t_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms, kern_ms = float(tt[0]), float(tt[1])
+    value = per * world * args.steps / (t_ms / 1e3)
+
+    # ---- end to end through the public host API: pinned host records -> H2D -> score -> winner D2H
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            w2 = dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        assert w2.global_index == win.global_index and w2.makespan_ns == win.makespan_ns
+        e2e = {"value": per * world * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": per * model.stride, "d2h_bytes_per_step": 8,
+               "path": "dip_eval_host: pinned host records, 64K-record chunks, H2D overlapped with scoring"}
+
+    hbm_peak, sm_max, src = peaks()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(pb, cs, args.cpu_sample, os.cpu_count() or 1)
+    if rank == 0:
+        clocks = clk.summary()
+        kern_s = kern_ms / 1e3
+        ops = INT_OPS_PER_STAGE * stages
+        alu_peak = INT_OPS_PER_CLK_SM * 148 * sm_max * 1e6
+        bytes_launch = per * (model.stride + 24 + 4 * pb.P)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("candidates_per_launch") == per:
+                traffic = tj.get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": config_block(args, pb, per, world),
+            "roofline": {"bound": "alu", "achieved": ops / kern_s / 1e12, "peak": alu_peak / 1e12,
+                         "unit": "Tintop/s", "frac": ops / kern_s / alu_peak, "traffic": traffic,
+                         "kernel": "dip_eval_kernel", "kernel_ms": kern_ms,
+                         "algorithmic": f"{INT_OPS_PER_STAGE} int32 ops x {stages} stage nodes per launch",
+                         "peak_source": f"128 int32 ops/clk/SM x 148 SMs x {sm_max:.0f} MHz ({src} sm_max)"},
+            "hbm": {"achieved": bytes_launch / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": bytes_launch / kern_s / 1e9 / hbm_peak,
+                    "algorithmic": "record + 24 B result + 4P B peaks per candidate", "peak_source": src},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
+            "status_hist": {"ok": hist[0], "oom": hist[1], "deadlock": hist[2], "bad_encoding": hist[3]},
+            "winner": {"found": win.found, "global_index": win.global_index, "makespan_ns": win.makespan_ns},
+            "setup_s": {"generate": round(t_gen, 1)},
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -13,12 +13,32 @@ DEPS = SRCS + [os.path.join(HERE, "csrc", "dip_internal.h"), os.path.join(ROOT, 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
+def _nccl_dirs():
+    """Link the NCCL that PyTorch itself loads (nvidia-nccl wheel), so that importing libdip before
+    torch cannot pin an older system libnccl.so.2 into the process."""
+    try:
+        import nvidia.nccl as nn
+        base = list(nn.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    except ImportError:
+        pass
+    return None, None
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in DEPS):
         return SO
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
-           *SRCS, "-o", SO, "-lnccl"]
+           *SRCS, "-o", SO]
+    inc, lib = _nccl_dirs()
+    if inc:
+        cmd[1:1] = ["-I", inc]
+        cmd += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
+    else:
+        cmd += ["-lnccl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

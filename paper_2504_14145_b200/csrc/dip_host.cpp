@@ -175,7 +175,7 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
         M->max_split.push_back(md.max_split);
         M->nib_slot.push_back(x.nib_slot);
     }
-    if (tab.size() / 4 > 65535 || layers.size() > 65535) return fail(DIP_ERANGE, "tables too large");
+    if (tab.size() / 4 > 4096 || layers.size() > 4096) return fail(DIP_ERANGE, "tables exceed the 12-bit row indices");
 
     // ---- segment ids, decode table, per-(b,i) base, balanced-split work table (R-2)
     uint32_t n_max = 0;
@@ -187,7 +187,7 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
             for (uint32_t j = 0; j < mi[i].max_split; j++)
                 for (uint32_t k = 0; k < mi[i].K; k++) segdec.push_back(dipk::segdec_pack(b, i, j, k, mi[i].K));
             n_max += mi[i].max_split * mi[i].K;
-            if (n_max > 65534) return fail(DIP_ERANGE, "segment-id space exceeds 65534");
+            if (n_max > 32766) return fail(DIP_ERANGE, "segment-id space exceeds 32766");
         }
     std::vector<uint32_t> woff(m * nm);
     std::vector<uint16_t> wtab, nbi(m * nm);
@@ -262,13 +262,13 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     M->cpg = 32 / G;
     uint32_t go = 0;
     auto gput = [&](uint32_t bytes) { const uint32_t o = go; go = up16(go + bytes); return o; };
-    kp.g_seqF = gput(2 * M->n_pad);
-    kp.g_seqB = gput(2 * M->n_pad);
-    kp.g_posF = gput(4 * n_max);
-    kp.g_posB = gput(4 * n_max);
-    kp.g_depF0 = gput(8 * n_max);
-    kp.g_depBP = gput(std::max<uint32_t>(8 * n_max, 8 * ((n_max + 31) / 32)));
-    kp.g_ring = gput(std::max<uint32_t>(2 * P * dipk::RING_D * 8, 4 * n_max));
+    // per-candidate working set: per-position rows [2][n_max] uint2 (validation bitmaps alias it),
+    // wrap slots [2][n_max] u64 (the decode copy of the sequences aliases it), channel rings
+    // [2][P][RING_D] u64, and M / producer / consumer counts per (b, i)
+    kp.g_seqF = kp.g_seqB = kp.g_posB = kp.g_depBP = 0;
+    kp.g_posF = gput(std::max<uint32_t>(16 * n_max, 8 * ((n_max + 31) / 32)));
+    kp.g_depF0 = gput(std::max<uint32_t>(16 * n_max + 16, 4 * M->n_pad));
+    kp.g_ring = gput(2 * P * dipk::RING_D * 8);
     kp.g_bmf = gput(3 * m * nm);
     kp.g_bytes = go;
 

@@ -72,12 +72,23 @@ __device__ __forceinline__ uint64_t group_sum(uint64_t v) {
 }
 
 // ------------------------------------------------------------------ the scorer -----------
+// Per-position entry (uint2), built at decode:
+//   x = tab_index (12 bits) | layer_row << 12 (12 bits) | flags << 24
+//   y = consume slot | publish slot << 16, both absolute indices into the wrap table
+//       depAll[2*n_max + 2] = [depF0 (n_max) | depBP (n_max) | ZERO | SINK]
+// F rows: rank 0 consumes its wrap slot, rank P-1 publishes end + p2p (chain / join) or, for the
+// loss turnaround (E_TURN), end - p2p into depBP so that the B consumer's uniform "+ p2p" cancels.
+// B rows: rank P-1 consumes (+ own p2p), rank 0 publishes end. Rows without a wrap dependency
+// consume ZERO (always ready, value 0); rows with nothing to publish write to SINK.
+constexpr uint32_t E_TURN = 1u << 24;     // F: publish target is the loss turnaround slot (R-6)
+constexpr uint32_t E_MULTI = 4u << 24;    // several join targets: slower loop (publish slot = segment id)
+
 template <int G>
 __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t blob_bar;
     constexpr int CPG = 32 / G;
-    constexpr int D = RING_D;
+    constexpr uint32_t D = RING_D;
     const unsigned FULL = 0xffffffffu;
 
     // (a1) static tables -> smem, one TMA bulk copy per CTA
@@ -104,23 +115,19 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
     const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (g * G));
     const uint32_t P = kp.P, nmod = kp.nmod, nq = kp.m * kp.nmod, n_max = kp.n_max;
     uint8_t *ga = smem + kp.blob_bytes + (size_t)(warp * CPG + g) * kp.g_bytes;
-    uint16_t *seqF = reinterpret_cast<uint16_t *>(ga + kp.g_seqF);
-    uint16_t *seqB = reinterpret_cast<uint16_t *>(ga + kp.g_seqB);
-    uint32_t *posF = reinterpret_cast<uint32_t *>(ga + kp.g_posF);
-    uint32_t *posB = reinterpret_cast<uint32_t *>(ga + kp.g_posB);
-    uint64_t *depF0 = reinterpret_cast<uint64_t *>(ga + kp.g_depF0);
-    uint64_t *depBP = reinterpret_cast<uint64_t *>(ga + kp.g_depBP);
-    uint64_t *ringF = reinterpret_cast<uint64_t *>(ga + kp.g_ring);
-    uint64_t *ringB = ringF + P * D;
-    uint32_t *segInfo = reinterpret_cast<uint32_t *>(ga + kp.g_ring);   // alias: decode only
-    uint32_t *bitmap = reinterpret_cast<uint32_t *>(ga + kp.g_depBP);   // alias: validation only
+    uint2 *posAll = reinterpret_cast<uint2 *>(ga + kp.g_posF);       // [2][n_max]: F then B
+    uint64_t *depAll = reinterpret_cast<uint64_t *>(ga + kp.g_depF0);  // [2][n_max]: depF0 then depBP
+    uint64_t *ringAll = reinterpret_cast<uint64_t *>(ga + kp.g_ring);  // [2][P][D]: F rings then B rings
+    uint16_t *seqF = reinterpret_cast<uint16_t *>(ga + kp.g_depF0);    // decode scratch (dep region)
+    uint16_t *seqB = seqF + kp.n_pad;
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(ga + kp.g_posF);   // validation scratch (pos region)
     uint8_t *Mb = ga + kp.g_bmf;          // M_{b,i}
     uint8_t *Pc = Mb + nq;                // present producer sub-microbatches of (b,i)
     uint8_t *Cc = Pc + nq;                // present consumer sub-microbatches of (b,i)
     const uint64_t slot_id = ((uint64_t)blockIdx.x * kp.warps_per_block + warp) * CPG + g;
-    unsigned long long *spF = kp.spill + slot_id * 2ull * P * n_max;
-    unsigned long long *spB = spF + (size_t)P * n_max;
+    unsigned long long *spill = kp.spill + slot_id * 2ull * P * n_max;   // [2][P][n_max]
     const uint32_t nwords = (n_max + 31) / 32;
+    const bool isFirst = r == 0, isLast = r == (int)P - 1, laneOn = r < (int)P;
 
     unsigned long long best = ~0ull;
 
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
             const uint32_t hi = N < Mx ? N : Mx;
             if ((N == 0) != (M == 0) || M > hi) bad = true;
-            Mb[q] = (uint8_t)(M > 15 ? 15 : M);
+            Mb[q] = (uint8_t)M;
             nsum += M * mi[i].K;
         }
         nsum = (uint32_t)group_sum<G>(nsum);
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             Pc[q] = (uint8_t)pc;
             Cc[q] = (uint8_t)cc;
         }
-        // sequences: 16-byte loads, copy to smem, check they are permutations of the present ids
+        // sequences: 16-byte loads, copy to smem scratch, check they are permutations of the present ids
         const uint32_t nv = kp.n_pad / 8;
         for (uint32_t v = r; v < nv; v += G) {
             const uint4 f4 = ldg128(rec + kp.off_fwd + 16 * v);
@@ -198,7 +205,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         }
         // F/B bit rows: exactly n ones in [0, 2n), zeros beyond
         uint32_t wcur = 0, wnext = 0;
-        if (r < (int)P) {
+        if (laneOn) {
             const uint32_t lim = 2 * n;
             uint32_t ones = 0;
             for (uint32_t w = 0; w < kp.fbw; w++) {
@@ -218,97 +225,113 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             if (ones != n) bad = true;
         }
         bad = (__ballot_sync(FULL, bad) & gmask) != 0;
-
-        // ---------------- K2: per-segment cost rows + wrap-dependency init ----------------
         __syncwarp();
+
+        // ---------------- K2: per-position cost rows and wrap-edge slots ----------------
+        const uint32_t ZS = 2 * n_max, SINK = 2 * n_max + 1;
         if (!bad) {
-            for (uint32_t s = r; s < n_max; s += G) {
+            for (uint32_t x = r; x < 2 * n; x += G) {
+                const bool hb = x >= n;
+                const uint32_t p = hb ? x - n : x;
+                const uint32_t s = hb ? seqB[p] : seqF[p];
                 const uint32_t dc = segdec[s];
                 const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
-                const uint32_t Km1 = dc >> 23, q = b * nmod + i, M = Mb[q];
-                uint64_t f0 = 0, bp = 0;
-                if (j < M) {
-                    const uint32_t W = wtab[woff[q] + M * (M - 1) / 2 + j];
-                    segInfo[s] = (mi[i].tab_off + W) | ((mi[i].lay_off + k * P) << 16);
-                    if (k > 0) f0 = 1ull << PEND_SHIFT;
-                    else if (j == 0) f0 = (uint64_t)Pc[q] << PEND_SHIFT;
-                    if (k < Km1) bp = 1ull << PEND_SHIFT;
-                    else if (Cc[q] == 0) bp = 1ull << PEND_SHIFT;            // loss turnaround (R-6)
-                    else if (j == 0) bp = (uint64_t)Cc[q] << PEND_SHIFT;     // consumer join (R-5)
+                const uint32_t K = (dc >> 23) + 1, q = b * nmod + i, M = Mb[q];
+                const uint32_t W = wtab[woff[q] + M * (M - 1) / 2 + j];
+                uint32_t ex = (mi[i].tab_off + W) | ((mi[i].lay_off + k * P) << 12);
+                uint32_t cs, ps;
+                if (!hb) {
+                    if (k > 0) cs = s;                              // previous segment, rank P-1 (R-4)
+                    else if (Pc[q]) cs = s - j * K;                 // producer join slot (R-5)
+                    else cs = ZS;
+                    if (k + 1 < K) ps = s + 1;
+                    else if (Cc[q] == 0) { ps = n_max + s; ex |= E_TURN; }   // loss turnaround (R-6)
+                    else {
+                        uint32_t cmods = 0, c1 = 0;
+                        for (uint32_t c = 0; c < nmod; c++)
+                            if (((mi[i].cons_mask >> c) & 1u) && Mb[b * nmod + c]) { cmods++; c1 = c; }
+                        if (cmods == 1) ps = sbase[b * nmod + c1];
+                        else { ps = s; ex |= E_MULTI; }
+                    }
+                } else {
+                    if (k + 1 < K) cs = n_max + s;                  // next segment, rank 0
+                    else if (Cc[q]) cs = n_max + s - j * K;         // consumer join slot id(b,i,0,K-1)
+                    else cs = n_max + s;                            // turnaround (same rank)
+                    if (k > 0) ps = n_max + s - 1;
+                    else {
+                        uint32_t pmods = 0, p1 = 0;
+                        for (uint32_t pp = 0; pp < nmod; pp++)
+                            if (((mi[i].prod_mask >> pp) & 1u) && Mb[b * nmod + pp]) { pmods++; p1 = pp; }
+                        if (pmods == 0) ps = SINK;
+                        else if (pmods == 1) ps = n_max + sbase[b * nmod + p1] + mi[p1].K - 1;
+                        else { ps = s; ex |= E_MULTI; }
+                    }
                 }
-                depF0[s] = f0;
-                depBP[s] = bp;
+                posAll[(hb ? n_max : 0) + p] = make_uint2(ex, cs | (ps << 16));
             }
         }
         __syncwarp();
-        if (!bad) {
-            for (uint32_t p = r; p < n; p += G) {
-                posF[p] = segInfo[seqF[p]];
-                posB[p] = segInfo[seqB[p]];
+        if (!bad) {   // wrap slots: pending counts in bits 56..63 (seq scratch is dead now)
+            for (uint32_t s = r; s < n_max; s += G) {
+                const uint32_t dc = segdec[s];
+                const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
+                const uint32_t Km1 = dc >> 23, q = b * nmod + i;
+                uint64_t f0 = 0, bp = 0;
+                if (j < Mb[q]) {
+                    if (k > 0) f0 = 1ull << PEND_SHIFT;
+                    else if (j == 0) f0 = (uint64_t)Pc[q] << PEND_SHIFT;
+                    if (k < Km1 || Cc[q] == 0) bp = 1ull << PEND_SHIFT;
+                    else if (j == 0) bp = (uint64_t)Cc[q] << PEND_SHIFT;
+                }
+                depAll[s] = f0;
+                depAll[n_max + s] = bp;
             }
+            if (r == 0) { depAll[ZS] = 0; depAll[SINK] = 0; }
         }
         __syncwarp();
 
         // ---------------- K3: lock-step wavefront longest path ----------------
+        // Channel rings are [2][D][P] u64 (F rings, then B rings; lane x owns column x), so the
+        // lanes of a round touch consecutive words: no bank conflicts beyond the 2 wavefronts
+        // of a 64-bit access.
         const uint32_t S2 = 2 * n;
-        bool done = bad || r >= (int)P || n == 0;
+        bool done = bad || !laneOn || n == 0;
         bool dl = false;
         uint32_t t = 0, fi = 0, bi = 0;
         uint64_t tlast = 0, busy = 0;
         uint32_t cur = 0, peak = 0;
+        const uint32_t colInF = (uint32_t)r - 1, colInB = P * D + r + 1;   // producer columns
+        const uint32_t colOutF = (uint32_t)r, colOutB = P * D + r;          // own columns
+        const uint32_t spInF = ((uint32_t)r - 1) * n_max, spInB = (P + r + 1) * n_max;
+        const uint32_t spOutF = (uint32_t)r * n_max, spOutB = (P + r) * n_max;
         for (;;) {
             const uint32_t packed = fi | (bi << 16);
             const uint32_t up = __shfl_up_sync(FULL, packed, 1, G);
             const uint32_t dn = __shfl_down_sync(FULL, packed, 1, G);
-            bool ready = false, isB = false;
-            uint64_t dep = 0;
-            uint32_t pos = 0, s = 0, dc = 0;
-            bool addp = false;
+            const bool isB = (wcur >> (t & 31)) & 1u;
+            const uint32_t idx = isB ? bi : fi;
+            const bool wrapC = isB ? isLast : isFirst;    // dependency comes through a wrap slot
+            const bool wrapP = isB ? isFirst : isLast;    // result goes into a wrap slot
+            uint32_t nb = isB ? (dn >> 16) : (up & 0xFFFFu);   // producer neighbour's count
+            nb = wrapC ? 0xFFFFu : nb;
+            const uint32_t cc = isB ? (up >> 16) : (dn & 0xFFFFu);   // consumer neighbour's count
+            const uint2 e = done ? make_uint2(0u, 0u) : posAll[(isB ? n_max : 0) + idx];   // done lanes: a safe row
+            const uint32_t ring = (idx & (D - 1)) * P;
+            const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (isB ? colInB : colInF)];
+            uint64_t *pa = wrapP ? &depAll[e.y >> 16] : &ringAll[ring + (isB ? colOutB : colOutF)];
+            const uint4 T = tab[e.x & 0xFFFu];
+            const uint32_t lay = layers[((e.x >> 12) & 0xFFFu) + r];
+            uint64_t v = 0, pold = 0;
             if (!done) {
-                isB = (wcur >> (t & 31)) & 1u;
-                if (!isB) {
-                    pos = posF[fi];
-                    if (r == 0) {                      // wrap / join edge from rank P-1 (R-4, R-5)
-                        s = seqF[fi];
-                        dc = segdec[s];
-                        const uint32_t j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF, K = (dc >> 23) + 1;
-                        const uint64_t v = depF0[k ? s : s - j * K];
-                        ready = (v >> PEND_SHIFT) == 0;
-                        dep = v & VAL_MASK;
-                    } else {                           // F(s, r-1) -> F(s, r)
-                        const uint32_t pf = up & 0xFFFFu;
-                        ready = pf > fi;
-                        if (ready) {
-                            dep = (fi + D >= pf) ? ringF[(r - 1) * D + (fi % D)] : spF[(r - 1) * n_max + fi];
-                            addp = true;
-                        }
-                    }
-                } else {
-                    pos = posB[bi];
-                    if (r == (int)P - 1) {             // wrap / join / turnaround edge from rank 0
-                        s = seqB[bi];
-                        dc = segdec[s];
-                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15;
-                        const uint32_t k = (dc >> 15) & 0xFF, Km1 = dc >> 23;
-                        uint32_t slot = s;
-                        addp = true;
-                        if (k == Km1) {
-                            if (Cc[b * nmod + i] == 0) addp = false;      // turnaround: same rank
-                            else slot = s - j * (Km1 + 1);                  // join slot id(b,i,0,K-1)
-                        }
-                        const uint64_t v = depBP[slot];
-                        ready = (v >> PEND_SHIFT) == 0;
-                        dep = v & VAL_MASK;
-                    } else {                           // B(s, r+1) -> B(s, r)
-                        const uint32_t pb = dn >> 16;
-                        ready = pb > bi;
-                        if (ready) {
-                            dep = (bi + D >= pb) ? ringB[(r + 1) * D + (bi % D)] : spB[(r + 1) * n_max + bi];
-                            addp = true;
-                        }
-                    }
-                }
+                v = *ca;
+                pold = *pa;
             }
+            const bool ready = !done && nb > idx && (v >> PEND_SHIFT) == 0;
+            const uint32_t w = (wrapC && !isB) ? 0u : T.w;
+            uint64_t dep = ((v & VAL_MASK) + w) & VAL_MASK;
+            if (ready && !wrapC && idx + D < nb)   // evicted from the channel ring: exact spill copy
+                dep = spill[(isB ? spInB : spInF) + idx] + w;
+
             const uint32_t prog = __ballot_sync(FULL, ready);
             const uint32_t alive = __ballot_sync(FULL, !done);
             if (alive == 0) break;
@@ -318,89 +341,54 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
             __syncwarp();
             if (ready) {
-                const uint4 T = tab[pos & 0xFFFFu];
-                const uint64_t lay = layers[(pos >> 16) + r];
-                const uint64_t lat = lay * (uint64_t)(isB ? T.y : T.x);
-                if (addp) dep += T.w;
+                const uint64_t lat = (uint64_t)lay * (isB ? T.y : T.x);
+                const uint32_t act = lay * T.z;
                 const uint64_t st = dep > tlast ? dep : tlast;
                 const uint64_t end = st + lat;
                 tlast = end;
                 busy += lat;
-                const uint32_t a = (uint32_t)lay * T.z;
-                if (!isB) {
-                    cur += a;
-                    peak = cur > peak ? cur : peak;
-                    if (r == (int)P - 1) {             // publish to rank 0 / the loss turnaround
-                        s = seqF[fi];
-                        dc = segdec[s];
+                cur = isB ? cur - act : cur + act;
+                peak = cur > peak ? cur : peak;
+                uint64_t val = end;
+                if (wrapP) {
+                    const uint64_t pv = (isB ? end : ((e.x & E_TURN) ? end - T.w : end + T.w)) & VAL_MASK;
+                    const uint64_t ov = pold & VAL_MASK;
+                    val = (pv > ov ? pv : ov) | (((pold >> PEND_SHIFT) - 1) << PEND_SHIFT);
+                    if (e.x & E_MULTI) {                 // several join targets (rare)
+                        const uint32_t s = e.y >> 16, dc = segdec[s];
                         const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
-                        const uint32_t k = (dc >> 15) & 0xFF, Km1 = dc >> 23;
-                        const uint64_t v = end + T.w;
-                        if (k < Km1) {
-                            depF0[s + 1] = v;
-                        } else {
-                            const uint32_t cm = mi[i].cons_mask;
-                            bool any = false;
-                            for (uint32_t c = 0; c < nmod; c++) {
-                                if (!((cm >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
-                                uint64_t *sl = &depF0[sbase[b * nmod + c]];
-                                const uint64_t old = *sl;
-                                const uint64_t ov = old & VAL_MASK;
-                                *sl = (v > ov ? v : ov) | (((old >> PEND_SHIFT) - 1) << PEND_SHIFT);
-                                any = true;
-                            }
-                            if (!any) depBP[s] = end;
+                        const uint32_t msk = isB ? mi[i].prod_mask : mi[i].cons_mask;
+                        for (uint32_t c = 0; c < nmod; c++) {
+                            if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                            uint64_t *sl = &depAll[isB ? n_max + sbase[b * nmod + c] + mi[c].K - 1 : sbase[b * nmod + c]];
+                            const uint64_t old = *sl, o2 = old & VAL_MASK;
+                            *sl = (pv > o2 ? pv : o2) | (((old >> PEND_SHIFT) - 1) << PEND_SHIFT);
                         }
-                    } else {                           // channel to rank r+1 (exact spill)
-                        const uint32_t nf = dn & 0xFFFFu;
-                        uint64_t *slot = &ringF[r * D + (fi % D)];
-                        if (fi >= D && nf + D <= fi) spF[r * n_max + fi - D] = *slot;
-                        *slot = end;
+                        pa = &depAll[SINK];
                     }
-                    fi++;
-                } else {
-                    cur -= a;
-                    if (r == 0) {                      // publish to rank P-1
-                        s = seqB[bi];
-                        dc = segdec[s];
-                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, k = (dc >> 15) & 0xFF;
-                        if (k > 0) {
-                            depBP[s - 1] = end;
-                        } else {
-                            const uint32_t pm = mi[i].prod_mask;
-                            for (uint32_t p = 0; p < nmod; p++) {
-                                if (!((pm >> p) & 1u) || Mb[b * nmod + p] == 0) continue;
-                                uint64_t *sl = &depBP[sbase[b * nmod + p] + mi[p].K - 1];
-                                const uint64_t old = *sl;
-                                const uint64_t ov = old & VAL_MASK;
-                                *sl = (end > ov ? end : ov) | (((old >> PEND_SHIFT) - 1) << PEND_SHIFT);
-                            }
-                        }
-                    } else {                           // channel to rank r-1
-                        const uint32_t nb = up >> 16;
-                        uint64_t *slot = &ringB[r * D + (bi % D)];
-                        if (bi >= D && nb + D <= bi) spB[r * n_max + bi - D] = *slot;
-                        *slot = end;
-                    }
-                    bi++;
+                } else if (idx >= D && cc + D <= idx) {  // consumer is >= D behind: keep the old entry
+                    spill[(isB ? spOutB : spOutF) + idx - D] = pold;
                 }
+                *pa = val;
+                fi += isB ? 0u : 1u;
+                bi += isB ? 1u : 0u;
                 t++;
                 if ((t & 31) == 0 && t < S2) {
                     wcur = wnext;
                     const uint32_t nw = (t >> 5) + 1;
                     if (nw < kp.fbw) wnext = ldg32(rec + kp.off_fb + 4 * (nw * P + r));
                 }
-                if (t == S2) done = true;
+                done = t == S2;
             }
             __syncwarp();
         }
         // deadlocked candidates: finish the order-only memory scan (R-9)
-        if (dl && r < (int)P) {
+        if (dl && laneOn) {
             while (t < S2) {
                 if ((t & 31) == 0 && t > 0) wcur = ldg32(rec + kp.off_fb + 4 * ((t >> 5) * P + r));
                 const bool b1 = (wcur >> (t & 31)) & 1u;
-                const uint32_t ps = b1 ? posB[bi++] : posF[fi++];
-                const uint32_t a = (uint32_t)layers[(ps >> 16) + r] * tab[ps & 0xFFFFu].z;
+                const uint2 ee = posAll[(b1 ? n_max + bi++ : fi++)];
+                const uint32_t a = (uint32_t)layers[((ee.x >> 12) & 0xFFFu) + r] * tab[ee.x & 0xFFFu].z;
                 if (!b1) { cur += a; peak = cur > peak ? cur : peak; }
                 else cur -= a;
                 t++;
