@@ -164,6 +164,14 @@ typedef struct {
 dip_status dip_argmin(const dip_model *m, dip_workspace *w, size_t count, uint64_t shard_stride,
                       uint32_t rank, uint32_t world, dip_comm *comm, dip_winner *out, void *stream);
 
+/* Host helpers of the cross-rank key (also what dip_argmin uses): key = makespan << (rbits+ibits)
+ * | rank << ibits | local, ibits = ceil(log2(shard_stride)), rbits = ceil(log2(world)) (both >= 1).
+ * The unsigned order of keys is the (makespan, global index) order under contiguous shards (R-15).
+ * dip_pack_key returns DIP_ERANGE if the makespan does not fit; UINT64_MAX unpacks to found = 0. */
+dip_status dip_pack_key(uint64_t makespan_ns, uint32_t rank, uint64_t local, uint64_t shard_stride, uint32_t world,
+                        uint64_t *key_out);
+dip_status dip_unpack_key(uint64_t key, uint64_t shard_stride, uint32_t world, dip_winner *out);
+
 /* End to end from HOST records (pinned for overlap): chunked H2D copies overlapped
  * with scoring, then dip_argmin. h_results ([count], host) may be NULL. Requires a
  * workspace created with host_chunk > 0. Synchronous. */

@@ -521,19 +521,7 @@ dip_status dip_argmin(const dip_model *M, dip_workspace *w, size_t count, uint64
         NCCL_TRY(ncclAllReduce(w->d_misc + 2, w->d_misc + 2, 1, ncclUint64, ncclMin, comm->comm, s));
         CUDA_TRY(cudaMemcpyAsync(w->h_misc, w->d_misc + 2, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
-        const unsigned long long k = w->h_misc[0];
-        out->found = k != ~0ull;
-        if (out->found) {
-            const uint64_t local = k & ((1ull << ibits) - 1);
-            out->rank = (int32_t)((k >> ibits) & ((1ull << rbits) - 1));
-            out->makespan_ns = k >> (ibits + rbits);
-            out->global_index = (uint64_t)out->rank * shard_stride + local;
-        } else {
-            out->rank = -1;
-            out->makespan_ns = ~0ull;
-            out->global_index = ~0ull;
-        }
-        return DIP_OK;
+        return dip_unpack_key(w->h_misc[0], shard_stride, world, out);
     }
     // exact fallback: min makespan, then min global index among ties (two allreduces)
     uint64_t mk, idx;
@@ -555,6 +543,36 @@ dip_status dip_argmin(const dip_model *M, dip_workspace *w, size_t count, uint64
     out->makespan_ns = gmk;
     out->global_index = w->h_misc[5];
     out->rank = out->found ? (int32_t)(w->h_misc[5] / shard_stride) : -1;
+    return DIP_OK;
+}
+
+// Cross-rank key layout: makespan << (rbits + ibits) | rank << ibits | local index,
+// ibits = bits(shard_stride), rbits = bits(world). Under contiguous shards the u64 order of keys is
+// the (makespan, global index) order (R-15). The device kernel make_gkey builds the same layout.
+dip_status dip_pack_key(uint64_t makespan_ns, uint32_t rank, uint64_t local, uint64_t shard_stride, uint32_t world,
+                        uint64_t *key_out) {
+    if (!key_out || world < 1 || rank >= world || local >= shard_stride) return fail(DIP_EINVAL, "bad argument");
+    const uint32_t ibits = bits_for(std::max<uint64_t>(shard_stride, 2)), rbits = bits_for(std::max<uint32_t>(world, 2));
+    if (ibits + rbits >= 63 || (makespan_ns >> (64 - ibits - rbits)) != 0)
+        return fail(DIP_ERANGE, "makespan does not fit the packed key");
+    *key_out = (makespan_ns << (rbits + ibits)) | ((uint64_t)rank << ibits) | local;
+    return DIP_OK;
+}
+
+dip_status dip_unpack_key(uint64_t key, uint64_t shard_stride, uint32_t world, dip_winner *out) {
+    if (!out || world < 1) return fail(DIP_EINVAL, "bad argument");
+    const uint32_t ibits = bits_for(std::max<uint64_t>(shard_stride, 2)), rbits = bits_for(std::max<uint32_t>(world, 2));
+    out->found = key != ~0ull;
+    if (out->found) {
+        const uint64_t local = key & ((1ull << ibits) - 1);
+        out->rank = (int32_t)((key >> ibits) & ((1ull << rbits) - 1));
+        out->makespan_ns = key >> (ibits + rbits);
+        out->global_index = (uint64_t)out->rank * shard_stride + local;
+    } else {
+        out->rank = -1;
+        out->makespan_ns = ~0ull;
+        out->global_index = ~0ull;
+    }
     return DIP_OK;
 }
 

@@ -88,12 +88,15 @@ def lib():
                              ctypes.POINTER(_Winner), vp]
     L.dip_eval_host.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                 vp, ctypes.POINTER(_Winner), vp]
+    L.dip_pack_key.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                               ctypes.POINTER(ctypes.c_uint64)]
+    L.dip_unpack_key.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_Winner)]
     L.dip_comm_unique_id.argtypes = [vp]
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
     for f in ("dip_load_cost_model", "dip_model_free", "dip_model_get_info", "dip_encode_candidates",
               "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_argmin", "dip_eval_host",
-              "dip_comm_unique_id", "dip_comm_init", "dip_comm_free"):
+              "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key"):
         getattr(L, f).restype = st
     L.dip_launch_count.restype = ctypes.c_uint64
     L.dip_launch_count.argtypes = []
@@ -263,6 +266,19 @@ def eval_host(model: Model, ws: Workspace, h_records, count: int, h_results=None
     _check(lib().dip_eval_host(model.handle, ws.handle, _ptr(h_records), count, _ptr(h_results),
                                shard_stride if shard_stride is not None else count, rank, world,
                                comm.handle if comm else None, ctypes.byref(w), _stream(stream)), "dip_eval_host")
+    return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
+
+
+def pack_key(makespan_ns: int, rank: int, local: int, shard_stride: int, world: int) -> int:
+    """Cross-rank argmin key (host side of dip_argmin's packed allreduce)."""
+    k = ctypes.c_uint64()
+    _check(lib().dip_pack_key(makespan_ns, rank, local, shard_stride, world, ctypes.byref(k)), "dip_pack_key")
+    return k.value
+
+
+def unpack_key(key: int, shard_stride: int, world: int) -> Winner:
+    w = _Winner()
+    _check(lib().dip_unpack_key(key, shard_stride, world, ctypes.byref(w)), "dip_unpack_key")
     return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
 
 
