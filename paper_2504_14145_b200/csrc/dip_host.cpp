@@ -215,6 +215,29 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
             }
         }
 
+    // ---- compact wrap slots (only segments that can ever own a wrap dependency get one):
+    // F slot: rank 0's forward waits on rank P-1 -- segments with k > 0, and the join base
+    //         (j = 0, k = 0) of modules with a producer that has instances in this microbatch;
+    // B slot: rank P-1's backward waits on rank 0 or on its own forward -- segments with k < K-1,
+    //         the join base (j = 0, k = K-1) and, when no consumer has instances here, every
+    //         last segment (loss turnaround, R-6).
+    std::vector<uint16_t> slotF(n_max, 0xFFFF), slotB(n_max, 0xFFFF);
+    uint32_t nslotF = 0, nslotB = 0;
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            bool prod_any = false, cons_any = false;
+            for (uint32_t x = 0; x < nm; x++) {
+                if (((mi[i].prod_mask >> x) & 1u) && nbi[b * nm + x]) prod_any = true;
+                if (((mi[i].cons_mask >> x) & 1u) && nbi[b * nm + x]) cons_any = true;
+            }
+            for (uint32_t j = 0; j < mi[i].max_split; j++)
+                for (uint32_t k = 0; k < mi[i].K; k++) {
+                    const uint32_t id = sbase[b * nm + i] + j * mi[i].K + k;
+                    if (k > 0 || (j == 0 && prod_any)) slotF[id] = (uint16_t)nslotF++;
+                    if (k + 1 < mi[i].K || j == 0 || !cons_any) slotB[id] = (uint16_t)nslotB++;
+                }
+        }
+
     // ---- overflow guards (DIP_ERANGE)
     const uint64_t nodes = (uint64_t)P * 2ull * n_max;
     const unsigned __int128 bound = (unsigned __int128)nodes * ((unsigned __int128)maxlat_layers * maxlat + maxp2p);
@@ -241,6 +264,10 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     kp.b_nbi = put(nbi.data(), nbi.size() * 2);
     kp.b_sbase = put(sbase.data(), sbase.size() * 2);
     kp.b_budget = put(d->budget_kib, P * 4);
+    kp.b_slotF = put(slotF.data(), slotF.size() * 2);
+    kp.b_slotB = put(slotB.data(), slotB.size() * 2);
+    kp.nslotF = nslotF;
+    kp.nslotB = nslotB;
     blob.resize(up16((uint32_t)blob.size()));
     kp.blob_bytes = (uint32_t)blob.size();
 
@@ -267,7 +294,7 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     // [2][P][RING_D] u64, and M / producer / consumer counts per (b, i)
     kp.g_seqF = kp.g_seqB = kp.g_posB = kp.g_depBP = 0;
     kp.g_posF = gput(std::max<uint32_t>(16 * n_max, 8 * ((n_max + 31) / 32)));
-    kp.g_depF0 = gput(std::max<uint32_t>(16 * n_max + 16, 4 * M->n_pad));
+    kp.g_depF0 = gput(std::max<uint32_t>(8 * (nslotF + nslotB + 2), 4 * M->n_pad));
     kp.g_ring = gput(2 * P * dipk::RING_D * 8);
     kp.g_bmf = gput(3 * m * nm);
     kp.g_bytes = go;

@@ -8,7 +8,7 @@
 
 namespace dipk {
 
-constexpr int RING_D = 8;              // depth of the smem inter-rank channels (spill beyond)
+constexpr int RING_D = 4;              // depth of the smem inter-rank channels (exact spill beyond)
 constexpr uint64_t PEND_SHIFT = 56;    // wrap-dependency slot: pending count in bits 56..63
 constexpr uint64_t VAL_MASK = (1ull << PEND_SHIFT) - 1;
 
@@ -30,7 +30,8 @@ struct KParams {
     // static tables, one contiguous 16-B aligned blob staged to smem by a TMA bulk copy
     const uint8_t *blob;
     uint32_t blob_bytes;   // multiple of 16
-    uint32_t b_modinfo, b_segdec, b_layers, b_tab, b_woff, b_wtab, b_nbi, b_sbase, b_budget;
+    uint32_t b_modinfo, b_segdec, b_layers, b_tab, b_woff, b_wtab, b_nbi, b_sbase, b_budget, b_slotF, b_slotB;
+    uint32_t nslotF, nslotB;   // compact wrap-slot counts: depAll = [F slots | B slots | ZERO | SINK]
     // per-candidate shared-memory working set (byte offsets inside a group area)
     uint32_t g_seqF, g_seqB, g_posF, g_posB, g_depF0, g_depBP, g_ring, g_bmf, g_bytes;
     uint32_t warps_per_block, cpg;

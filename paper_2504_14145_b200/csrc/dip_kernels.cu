@@ -75,7 +75,8 @@ __device__ __forceinline__ uint64_t group_sum(uint64_t v) {
 // Per-position entry (uint2), built at decode:
 //   x = tab_index (12 bits) | layer_row << 12 (12 bits) | flags << 24
 //   y = consume slot | publish slot << 16, both absolute indices into the wrap table
-//       depAll[2*n_max + 2] = [depF0 (n_max) | depBP (n_max) | ZERO | SINK]
+//       (E_MULTI rows: publish field = SINK + 1 + segment id; the plain store is clamped to SINK)
+//       depAll = [F slots (nslotF) | B slots (nslotB) | ZERO | SINK] (compact, host-assigned)
 // F rows: rank 0 consumes its wrap slot, rank P-1 publishes end + p2p (chain / join) or, for the
 // loss turnaround (E_TURN), end - p2p into depBP so that the B consumer's uniform "+ p2p" cancels.
 // B rows: rank P-1 consumes (+ own p2p), rank 0 publishes end. Rows without a wrap dependency
@@ -109,6 +110,9 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
     const uint16_t *nbi = reinterpret_cast<const uint16_t *>(smem + kp.b_nbi);
     const uint16_t *sbase = reinterpret_cast<const uint16_t *>(smem + kp.b_sbase);
     const uint32_t *budget = reinterpret_cast<const uint32_t *>(smem + kp.b_budget);
+    const uint16_t *slotF = reinterpret_cast<const uint16_t *>(smem + kp.b_slotF);   // compact wrap slots
+    const uint16_t *slotB = reinterpret_cast<const uint16_t *>(smem + kp.b_slotB);
+    const uint32_t nF = kp.nslotF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane / G, r = lane % G;
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         __syncwarp();
 
         // ---------------- K2: per-position cost rows and wrap-edge slots ----------------
-        const uint32_t ZS = 2 * n_max, SINK = 2 * n_max + 1;
+        const uint32_t ZS = kp.nslotF + kp.nslotB, SINK = ZS + 1;
         if (!bad) {
             for (uint32_t x = r; x < 2 * n; x += G) {
                 const bool hb = x >= n;
@@ -241,30 +245,30 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 uint32_t ex = (mi[i].tab_off + W) | ((mi[i].lay_off + k * P) << 12);
                 uint32_t cs, ps;
                 if (!hb) {
-                    if (k > 0) cs = s;                              // previous segment, rank P-1 (R-4)
-                    else if (Pc[q]) cs = s - j * K;                 // producer join slot (R-5)
+                    if (k > 0) cs = slotF[s];                       // previous segment, rank P-1 (R-4)
+                    else if (Pc[q]) cs = slotF[s - j * K];          // producer join slot (R-5)
                     else cs = ZS;
-                    if (k + 1 < K) ps = s + 1;
-                    else if (Cc[q] == 0) { ps = n_max + s; ex |= E_TURN; }   // loss turnaround (R-6)
+                    if (k + 1 < K) ps = slotF[s + 1];
+                    else if (Cc[q] == 0) { ps = nF + slotB[s]; ex |= E_TURN; }   // loss turnaround (R-6)
                     else {
                         uint32_t cmods = 0, c1 = 0;
                         for (uint32_t c = 0; c < nmod; c++)
                             if (((mi[i].cons_mask >> c) & 1u) && Mb[b * nmod + c]) { cmods++; c1 = c; }
-                        if (cmods == 1) ps = sbase[b * nmod + c1];
-                        else { ps = s; ex |= E_MULTI; }
+                        if (cmods == 1) ps = slotF[sbase[b * nmod + c1]];
+                        else { ps = SINK + 1 + s; ex |= E_MULTI; }
                     }
                 } else {
-                    if (k + 1 < K) cs = n_max + s;                  // next segment, rank 0
-                    else if (Cc[q]) cs = n_max + s - j * K;         // consumer join slot id(b,i,0,K-1)
-                    else cs = n_max + s;                            // turnaround (same rank)
-                    if (k > 0) ps = n_max + s - 1;
+                    if (k + 1 < K) cs = nF + slotB[s];              // next segment, rank 0
+                    else if (Cc[q]) cs = nF + slotB[s - j * K];     // consumer join slot id(b,i,0,K-1)
+                    else cs = nF + slotB[s];                        // turnaround (same rank)
+                    if (k > 0) ps = nF + slotB[s - 1];
                     else {
                         uint32_t pmods = 0, p1 = 0;
                         for (uint32_t pp = 0; pp < nmod; pp++)
                             if (((mi[i].prod_mask >> pp) & 1u) && Mb[b * nmod + pp]) { pmods++; p1 = pp; }
                         if (pmods == 0) ps = SINK;
-                        else if (pmods == 1) ps = n_max + sbase[b * nmod + p1] + mi[p1].K - 1;
-                        else { ps = s; ex |= E_MULTI; }
+                        else if (pmods == 1) ps = nF + slotB[sbase[b * nmod + p1] + mi[p1].K - 1];
+                        else { ps = SINK + 1 + s; ex |= E_MULTI; }
                     }
                 }
                 posAll[(hb ? n_max : 0) + p] = make_uint2(ex, cs | (ps << 16));
@@ -276,61 +280,61 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 const uint32_t dc = segdec[s];
                 const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
                 const uint32_t Km1 = dc >> 23, q = b * nmod + i;
-                uint64_t f0 = 0, bp = 0;
-                if (j < Mb[q]) {
-                    if (k > 0) f0 = 1ull << PEND_SHIFT;
-                    else if (j == 0) f0 = (uint64_t)Pc[q] << PEND_SHIFT;
-                    if (k < Km1 || Cc[q] == 0) bp = 1ull << PEND_SHIFT;
-                    else if (j == 0) bp = (uint64_t)Cc[q] << PEND_SHIFT;
+                const bool pres = j < Mb[q];
+                if (slotF[s] != 0xFFFFu) {
+                    uint64_t f0 = 0;
+                    if (pres) f0 = (k > 0 ? 1ull : (uint64_t)Pc[q]) << PEND_SHIFT;
+                    depAll[slotF[s]] = f0;
                 }
-                depAll[s] = f0;
-                depAll[n_max + s] = bp;
+                if (slotB[s] != 0xFFFFu) {
+                    uint64_t bp = 0;
+                    if (pres) bp = ((k < Km1 || Cc[q] == 0) ? 1ull : (uint64_t)Cc[q]) << PEND_SHIFT;
+                    depAll[nF + slotB[s]] = bp;
+                }
             }
             if (r == 0) { depAll[ZS] = 0; depAll[SINK] = 0; }
         }
         __syncwarp();
 
         // ---------------- K3: lock-step wavefront longest path ----------------
-        // Channel rings are [2][D][P] u64 (F rings, then B rings; lane x owns column x), so the
-        // lanes of a round touch consecutive words: no bank conflicts beyond the 2 wavefronts
-        // of a 64-bit access.
+        // Per round every lane of the group tries its next slot (F if bit t is 0, else B):
+        // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
+        // P-1 for B, from a wrap slot), end = max(t_last, dep + p2p) + layers * lat, then publish
+        // end into its own channel ring (or read-modify-write a wrap slot). The F and B state is
+        // indexed by isB with shifts (counts packed as fi | bi << 16) rather than selects.
+        // Channel rings are [2][D][P] u64 (F rings, then B rings; lane x owns column x).
         const uint32_t S2 = 2 * n;
         bool done = bad || !laneOn || n == 0;
         bool dl = false;
-        uint32_t t = 0, fi = 0, bi = 0;
+        uint32_t t = 0, cnt = 0;                 // cnt = fi | bi << 16
         uint64_t tlast = 0, busy = 0;
         uint32_t cur = 0, peak = 0;
-        const uint32_t colInF = (uint32_t)r - 1, colInB = P * D + r + 1;   // producer columns
-        const uint32_t colOutF = (uint32_t)r, colOutB = P * D + r;          // own columns
-        const uint32_t spInF = ((uint32_t)r - 1) * n_max, spInB = (P + r + 1) * n_max;
-        const uint32_t spOutF = (uint32_t)r * n_max, spOutB = (P + r) * n_max;
+        const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
+        const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
+        const uint32_t wrapBits = (isFirst ? 1u : 0u) | (isLast ? 2u : 0u);   // bit d: consumes dir d via wrap
+        const uint32_t wrapPub = (isLast ? 1u : 0u) | (isFirst ? 2u : 0u);    // bit d: publishes dir d via wrap
         for (;;) {
-            const uint32_t packed = fi | (bi << 16);
-            const uint32_t up = __shfl_up_sync(FULL, packed, 1, G);
-            const uint32_t dn = __shfl_down_sync(FULL, packed, 1, G);
-            const bool isB = (wcur >> (t & 31)) & 1u;
-            const uint32_t idx = isB ? bi : fi;
-            const bool wrapC = isB ? isLast : isFirst;    // dependency comes through a wrap slot
-            const bool wrapP = isB ? isFirst : isLast;    // result goes into a wrap slot
-            uint32_t nb = isB ? (dn >> 16) : (up & 0xFFFFu);   // producer neighbour's count
-            nb = wrapC ? 0xFFFFu : nb;
-            const uint32_t cc = isB ? (up >> 16) : (dn & 0xFFFFu);   // consumer neighbour's count
-            const uint2 e = done ? make_uint2(0u, 0u) : posAll[(isB ? n_max : 0) + idx];   // done lanes: a safe row
+            const uint32_t up = __shfl_up_sync(FULL, cnt, 1, G);
+            const uint32_t dn = __shfl_down_sync(FULL, cnt, 1, G);
+            const uint32_t d = (wcur >> (t & 31)) & 1u;            // 0 = F, 1 = B
+            const uint32_t sh = d << 4;
+            const uint32_t idx = (cnt >> sh) & 0xFFFFu;
+            const bool wrapC = (wrapBits >> d) & 1u;
+            const bool wrapP = (wrapPub >> d) & 1u;
+            const uint32_t nb = wrapC ? 0xFFFFu : (((d ? dn : up) >> sh) & 0xFFFFu);   // producer's count
+            const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];       // done lanes: a safe row
             const uint32_t ring = (idx & (D - 1)) * P;
-            const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (isB ? colInB : colInF)];
-            uint64_t *pa = wrapP ? &depAll[e.y >> 16] : &ringAll[ring + (isB ? colOutB : colOutF)];
+            const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (d ? colIn1 : colIn0)];
+            uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)] : &ringAll[ring + (d ? colOut1 : colOut0)];
             const uint4 T = tab[e.x & 0xFFFu];
             const uint32_t lay = layers[((e.x >> 12) & 0xFFFu) + r];
-            uint64_t v = 0, pold = 0;
-            if (!done) {
-                v = *ca;
-                pold = *pa;
-            }
+            const uint64_t v = *ca;
+            const uint64_t pold = *pa;
             const bool ready = !done && nb > idx && (v >> PEND_SHIFT) == 0;
-            const uint32_t w = (wrapC && !isB) ? 0u : T.w;
-            uint64_t dep = ((v & VAL_MASK) + w) & VAL_MASK;
+            const uint32_t w = (wrapC && !d) ? 0u : T.w;   // rank 0's F wrap slot already holds + p2p
+            uint64_t dep = (v + w) & VAL_MASK;
             if (ready && !wrapC && idx + D < nb)   // evicted from the channel ring: exact spill copy
-                dep = spill[(isB ? spInB : spInF) + idx] + w;
+                dep = spill[(d ? (P + r + 1) : (r - 1)) * n_max + idx] + w;
 
             const uint32_t prog = __ballot_sync(FULL, ready);
             const uint32_t alive = __ballot_sync(FULL, !done);
@@ -341,39 +345,39 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
             __syncwarp();
             if (ready) {
-                const uint64_t lat = (uint64_t)lay * (isB ? T.y : T.x);
+                const uint64_t lat = (uint64_t)lay * (d ? T.y : T.x);
                 const uint32_t act = lay * T.z;
                 const uint64_t st = dep > tlast ? dep : tlast;
                 const uint64_t end = st + lat;
                 tlast = end;
                 busy += lat;
-                cur = isB ? cur - act : cur + act;
+                cur = d ? cur - act : cur + act;
                 peak = cur > peak ? cur : peak;
-                uint64_t val = end;
-                if (wrapP) {
-                    const uint64_t pv = (isB ? end : ((e.x & E_TURN) ? end - T.w : end + T.w)) & VAL_MASK;
-                    const uint64_t ov = pold & VAL_MASK;
-                    val = (pv > ov ? pv : ov) | (((pold >> PEND_SHIFT) - 1) << PEND_SHIFT);
-                    if (e.x & E_MULTI) {                 // several join targets (rare)
-                        const uint32_t s = e.y >> 16, dc = segdec[s];
-                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
-                        const uint32_t msk = isB ? mi[i].prod_mask : mi[i].cons_mask;
-                        for (uint32_t c = 0; c < nmod; c++) {
-                            if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
-                            uint64_t *sl = &depAll[isB ? n_max + sbase[b * nmod + c] + mi[c].K - 1 : sbase[b * nmod + c]];
-                            const uint64_t old = *sl, o2 = old & VAL_MASK;
-                            *sl = (pv > o2 ? pv : o2) | (((old >> PEND_SHIFT) - 1) << PEND_SHIFT);
-                        }
-                        pa = &depAll[SINK];
+                // wrap publish value: F -> end + p2p (chain / join), or end - p2p for the loss turnaround
+                // (its B consumer adds p2p back); B -> end
+                const int64_t pw = d ? 0 : ((e.x & E_TURN) ? -(int64_t)T.w : (int64_t)T.w);
+                const uint64_t pv = (end + (uint64_t)pw) & VAL_MASK;
+                const uint64_t ov = pold & VAL_MASK;
+                const uint64_t rmw = (pv > ov ? pv : ov) | ((pold & ~VAL_MASK) - (1ull << PEND_SHIFT));
+                *pa = wrapP ? rmw : end;
+                if (!wrapP) {
+                    const uint32_t cc = ((d ? up : dn) >> sh) & 0xFFFFu;   // consumer neighbour's count
+                    if (idx >= D && cc + D <= idx)        // consumer is >= D behind: keep the old entry
+                        spill[(d ? (P + r) : r) * n_max + idx - D] = pold;
+                } else if (e.x & E_MULTI) {               // several join targets (rare); the plain store hit SINK
+                    const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
+                    const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
+                    const uint32_t msk = d ? mi[i].prod_mask : mi[i].cons_mask;
+                    for (uint32_t c = 0; c < nmod; c++) {
+                        if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                        uint64_t *sl = &depAll[d ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
+                        const uint64_t old = *sl, o2 = old & VAL_MASK;
+                        *sl = (pv > o2 ? pv : o2) | ((old & ~VAL_MASK) - (1ull << PEND_SHIFT));
                     }
-                } else if (idx >= D && cc + D <= idx) {  // consumer is >= D behind: keep the old entry
-                    spill[(isB ? spOutB : spOutF) + idx - D] = pold;
                 }
-                *pa = val;
-                fi += isB ? 0u : 1u;
-                bi += isB ? 1u : 0u;
+                cnt += 1u << sh;
                 t++;
-                if ((t & 31) == 0 && t < S2) {
+                if ((t & 31) == 0) {
                     wcur = wnext;
                     const uint32_t nw = (t >> 5) + 1;
                     if (nw < kp.fbw) wnext = ldg32(rec + kp.off_fb + 4 * (nw * P + r));
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
             __syncwarp();
         }
+        uint32_t fi = cnt & 0xFFFFu, bi = cnt >> 16;
         // deadlocked candidates: finish the order-only memory scan (R-9)
         if (dl && laneOn) {
             while (t < S2) {
