@@ -283,11 +283,10 @@ def main():
         bytes_launch = per * (model.stride + 24 + 4 * pb.P)
         traffic = None
         tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp):   # DRAM bytes per candidate from the committed ncu --set full capture
             with open(tp) as f:
                 tj = json.load(f)
-            if tj.get("candidates_per_launch") == per:
-                traffic = tj.get("dram_bytes_per_launch")
+            traffic = tj["dram_bytes_per_candidate"] * per
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -295,6 +294,8 @@ def main():
             "config": config_block(args, pb, per, world),
             "roofline": {"bound": "alu", "achieved": ops / kern_s / 1e12, "peak": alu_peak / 1e12,
                          "unit": "Tintop/s", "frac": ops / kern_s / alu_peak, "traffic": traffic,
+                         "traffic_source": "profiles/ncu_traffic_%s.json (per-candidate DRAM bytes x candidates per launch)" % args.config,
+                         "algorithmic_bytes": bytes_launch,
                          "kernel": "dip_eval_kernel", "kernel_ms": kern_ms,
                          "algorithmic": f"{INT_OPS_PER_STAGE} int32 ops x {stages} stage nodes per launch",
                          "peak_source": f"128 int32 ops/clk/SM x 148 SMs x {sm_max:.0f} MHz ({src} sm_max)"},
