@@ -68,6 +68,7 @@ typedef struct {
     uint32_t *segs_mb, *infl, *cons;
     uint64_t *fk;
     uint32_t *posf, *posb, *perm;
+    uint8_t *newmb, *endmb;
 } scratch_t;
 
 static void heap_push(scratch_t *w, uint32_t *hn, uint64_t key, uint32_t id) {
@@ -174,20 +175,18 @@ static void linear_extension(const gen_cfg *c, scratch_t *w, int dir, const uint
 }
 
 /* Dependency-readiness replay: decides each rank's F/B bit string.  A rank may
- * start the forward of a *new* microbatch only while fewer than cap_r microbatches
- * are in flight on it (memory gating in microbatch units; 1F1B = P - r).  If no rank
- * can act, the caps are relaxed for one round.  Returns 0 on success (always, for
- * linear-extension sequences). */
+ * start the forward of a *new* microbatch (its first backbone segment) only while
+ * fewer than cap_r microbatches are in flight on it (memory gating in microbatch
+ * units; 1F1B = P - r).  If no rank can act, the caps are relaxed for one round.
+ * Returns 0 on success (always, for linear-extension sequences). */
 static int readiness_bits(const gen_cfg *c, scratch_t *w, uint32_t n, const uint16_t *fwd,
                           const uint16_t *bwd, int ffirst, uint32_t *fb /* [P][fbw] */) {
-    const uint32_t P = c->P, nm = c->nmod, m = c->m;
-    for (uint32_t b = 0; b < m; b++) {
+    const uint32_t P = c->P, nm = c->nmod;
+    for (uint32_t b = 0; b < c->m; b++) {
         uint32_t t = 0;
         for (uint32_t i = 0; i < nm; i++) if (!w->cons[i]) t += w->M[b * nm + i] * c->K[i];
         w->segs_mb[b] = t;
     }
-    memset(w->fmb, 0, sizeof(uint16_t) * P * m);
-    memset(w->bmb, 0, sizeof(uint16_t) * P * m);
     for (uint32_t id = 0; id < c->n_max; id++) {
         if (!w->present[id]) continue;
         uint32_t b = w->segb[id], i = w->segi[id], k = w->segk[id];
@@ -205,39 +204,50 @@ static int readiness_bits(const gen_cfg *c, scratch_t *w, uint32_t n, const uint
         w->cntF0[id] = f0;
         w->cntBP[id] = bp;
     }
+    /* per-position flags: newmb[p] = fwd[p] is the first backbone segment of its microbatch in
+     * forward order; endmb[p] = bwd[p] is the last backbone segment of its microbatch in
+     * backward order (a rank's in-flight microbatch count changes exactly there) */
+    for (uint32_t b = 0; b < c->m; b++) { w->fmb[b] = 0; w->bmb[b] = 0; }
+    for (uint32_t p = 0; p < n; p++) {
+        uint32_t s = fwd[p], bb = w->segb[s];
+        w->newmb[p] = (!w->cons[w->segi[s]] && w->fmb[bb]++ == 0);
+    }
+    for (uint32_t p = 0; p < n; p++) {
+        uint32_t s = bwd[p], bb = w->segb[s];
+        w->endmb[p] = (!w->cons[w->segi[s]] && ++w->bmb[bb] == w->segs_mb[bb]);
+    }
+    w->newmb[n] = 0;
+    w->endmb[n] = 0;
     for (uint32_t r = 0; r < P; r++) { w->fi[r] = 0; w->bi[r] = 0; w->infl[r] = 0; }
     memset(fb, 0, sizeof(uint32_t) * P * c->fbw);
     uint32_t remaining = P * 2 * n;
-    int relax = 0;
+    uint32_t relax = 0;
+    uint32_t *fi = w->fi, *bi = w->bi, *infl = w->infl, *cap = w->cap;
+    /* one fused sweep per lock-step round: rank r decides on the start-of-round state (fi[r-1] is
+     * carried in `fprev` before rank r-1's update; bi[r+1] and cntF0 are not yet updated when read;
+     * rank 0's backward publications to cntBP are deferred until after rank P-1 decided) */
     while (remaining) {
-        uint32_t acted = 0;
+        uint32_t acted = 0, fprev = 0, defer_s = 0xFFFFFFFFu;
         for (uint32_t r = 0; r < P; r++) {
-            uint32_t fr = w->fi[r], br = w->bi[r];
-            int frdy = fr < n && (r > 0 ? w->fi[r - 1] > fr : w->cntF0[fwd[fr]] == 0);
-            int brdy = br < n && (r + 1 < P ? w->bi[r + 1] > br : w->cntBP[bwd[br]] == 0);
-            int under = relax || (frdy && (w->cons[w->segi[fwd[fr]]] || w->fmb[r * m + w->segb[fwd[fr]]] > 0 || w->infl[r] < w->cap[r]));
-            uint8_t d = 0;
-            if (ffirst) d = (frdy && under) ? 1 : (brdy ? 2 : 0);
-            else d = brdy ? 2 : ((frdy && under) ? 1 : 0);
-            w->dec[r] = d;
-            acted += d != 0;
-        }
-        if (!acted) {
-            if (relax) return -1;
-            relax = 1;
-            continue;
-        }
-        relax = 0;
-        for (uint32_t r = 0; r < P; r++) {
-            uint8_t d = w->dec[r];
+            const uint32_t fr = fi[r], br = bi[r];
+            uint32_t frdy, brdy;
+            if (r == 0) frdy = fr < n && w->cntF0[fwd[fr]] == 0;
+            else frdy = (fr < n) & (fprev > fr);
+            if (r + 1 == P) brdy = br < n && w->cntBP[bwd[br]] == 0;
+            else brdy = (br < n) & (bi[r + 1] > br);
+            const uint32_t under = relax | (uint32_t)(w->newmb[fr] == 0) | (uint32_t)(infl[r] < cap[r]);
+            const uint32_t fok = frdy & under;
+            const uint32_t d = ffirst ? (fok ? 1u : 2u * brdy) : (brdy ? 2u : fok);
+            fprev = fr;
             if (!d) continue;
-            uint32_t t = w->fi[r] + w->bi[r];
+            acted = 1;
+            const uint32_t t = fr + br;
             if (d == 1) {
-                uint32_t s = fwd[w->fi[r]++];
-                uint32_t b = w->segb[s];
-                if (!w->cons[w->segi[s]] && w->fmb[r * m + b]++ == 0) w->infl[r]++;
+                fi[r] = fr + 1;
+                const uint32_t s = fwd[fr];
+                infl[r] += w->newmb[fr];
                 if (r == P - 1) {
-                    uint32_t i = w->segi[s], k = w->segk[s];
+                    uint32_t b = w->segb[s], i = w->segi[s], k = w->segk[s];
                     if (k + 1 < c->K[i]) w->cntF0[s + 1]--;
                     else {
                         uint32_t cm = w->cons[i], any = 0;
@@ -252,20 +262,28 @@ static int readiness_bits(const gen_cfg *c, scratch_t *w, uint32_t n, const uint
                 }
             } else {
                 fb[r * c->fbw + (t >> 5)] |= 1u << (t & 31);
-                uint32_t s = bwd[w->bi[r]++];
-                uint32_t b = w->segb[s];
-                if (!w->cons[w->segi[s]] && ++w->bmb[r * m + b] == w->segs_mb[b]) w->infl[r]--;
-                if (r == 0) {
-                    uint32_t i = w->segi[s], k = w->segk[s];
-                    if (k > 0) w->cntBP[s - 1]--;
-                    else for (uint32_t p = 0; p < nm; p++)
-                        if ((c->producer_mask[i] >> p) & 1u)
-                            for (uint32_t jj = 0; jj < w->M[b * nm + p]; jj++)
-                                w->cntBP[w->base[b * nm + p] + jj * c->K[p] + c->K[p] - 1]--;
-                }
+                bi[r] = br + 1;
+                const uint32_t s = bwd[br];
+                infl[r] -= w->endmb[br];
+                if (r == 0) defer_s = s;
             }
             remaining--;
         }
+        if (defer_s != 0xFFFFFFFFu) {   /* rank 0's backward publication (after rank P-1 decided) */
+            const uint32_t s = defer_s;
+            uint32_t b = w->segb[s], i = w->segi[s], k = w->segk[s];
+            if (k > 0) w->cntBP[s - 1]--;
+            else for (uint32_t pp = 0; pp < nm; pp++)
+                if ((c->producer_mask[i] >> pp) & 1u)
+                    for (uint32_t jj = 0; jj < w->M[b * nm + pp]; jj++)
+                        w->cntBP[w->base[b * nm + pp] + jj * c->K[pp] + c->K[pp] - 1]--;
+        }
+        if (!acted) {
+            if (relax) return -1;
+            relax = 1;
+            continue;
+        }
+        relax = 0;
     }
     return 0;
 }
@@ -479,6 +497,7 @@ static void *worker(void *arg) {
     w.segs_mb = malloc(sizeof(uint32_t) * (c->m + 1)); w.infl = malloc(sizeof(uint32_t) * c->P);
     w.cons = malloc(sizeof(uint32_t) * (c->nmod + 1)); w.fk = malloc(sizeof(uint64_t) * nmx);
     w.posf = malloc(sizeof(uint32_t) * (c->m + 1)); w.posb = malloc(sizeof(uint32_t) * (c->m + 1)); w.perm = malloc(sizeof(uint32_t) * (c->m + 1));
+    w.newmb = malloc(nmx + 1); w.endmb = malloc(nmx + 1);
     for (uint32_t i = 0; i < c->nmod; i++) w.cons[i] = consumers_of(c, i);
     for (uint64_t x = j->lo; x < j->hi; x++) {
         uint64_t o = x - j->first;
@@ -488,7 +507,7 @@ static void *worker(void *arg) {
     }
     free(w.segb); free(w.segi); free(w.segj); free(w.segk); free(w.present); free(w.indeg);
     free(w.heap_key); free(w.heap_id); free(w.prio); free(w.fpos); free(w.cntF0); free(w.cntBP);
-    free(w.fi); free(w.bi); free(w.cap); free(w.dec); free(w.base); free(w.M); free(w.fmb); free(w.bmb); free(w.segs_mb); free(w.infl); free(w.cons); free(w.fk); free(w.posf); free(w.posb); free(w.perm);
+    free(w.fi); free(w.bi); free(w.cap); free(w.dec); free(w.base); free(w.M); free(w.fmb); free(w.bmb); free(w.segs_mb); free(w.infl); free(w.cons); free(w.fk); free(w.posf); free(w.posb); free(w.perm); free(w.newmb); free(w.endmb);
     return NULL;
 }
 
