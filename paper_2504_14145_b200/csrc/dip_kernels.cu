@@ -78,11 +78,28 @@ __device__ __forceinline__ uint64_t group_sum(uint64_t v) {
 //       (E_MULTI rows: publish field = SINK + 1 + segment id; the plain store is clamped to SINK)
 //       depAll = [F slots (nslotF) | B slots (nslotB) | ZERO | SINK] (compact, host-assigned)
 // F rows: rank 0 consumes its wrap slot, rank P-1 publishes end + p2p (chain / join) or, for the
-// loss turnaround (E_TURN), end - p2p into depBP so that the B consumer's uniform "+ p2p" cancels.
+// loss turnaround, end - p2p into the B slot so that the B consumer's uniform "+ p2p" cancels.
 // B rows: rank P-1 consumes (+ own p2p), rank 0 publishes end. Rows without a wrap dependency
 // consume ZERO (always ready, value 0); rows with nothing to publish write to SINK.
-constexpr uint32_t E_TURN = 1u << 24;     // F: publish target is the loss turnaround slot (R-6)
-constexpr uint32_t E_MULTI = 4u << 24;    // several join targets: slower loop (publish slot = segment id)
+// bits 24-25: signed publish factor s in {-1, 0, +1}: a wrap publication writes end + s * p2p
+//   (F chain / join: +1; F loss turnaround: -1, its B consumer adds p2p back; B rows: 0)
+constexpr uint32_t E_SPLUS = 1u << 24;
+constexpr uint32_t E_SMINUS = 3u << 24;
+constexpr uint32_t E_MULTI = 4u << 24;    // several join targets: slower loop (publish slot = SINK + 1 + segment id)
+// Wrap slots: value in bits 0..55; bits 56..63 = (256 - producers still to come) mod 256, so a slot is
+// ready when its top byte is 0, and a producer publishes with one 64-bit max and one add:
+//   slot = max(slot, (slot & HIGH) | value) + (1 << 56)
+constexpr uint64_t HIGH_MASK = ~VAL_MASK;
+
+// rare paths kept out of line (a call is never if-converted into the round's common path)
+__device__ __noinline__ uint64_t spill_load(const unsigned long long *spill, uint32_t d, uint32_t r, uint32_t P,
+                                            uint32_t n_max, uint32_t idx) {
+    return spill[(d ? (P + r + 1) : (r - 1)) * n_max + idx];
+}
+__device__ __noinline__ void spill_keep(unsigned long long *spill, uint32_t d, uint32_t r, uint32_t P,
+                                        uint32_t n_max, uint32_t idx, uint64_t v) {
+    spill[(d ? (P + r) : r) * n_max + idx - RING_D] = v;
+}
 
 template <int G>
 __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
@@ -245,11 +262,12 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 uint32_t ex = (mi[i].tab_off + W) | ((mi[i].lay_off + k * P) << 12);
                 uint32_t cs, ps;
                 if (!hb) {
+                    ex |= E_SPLUS;
                     if (k > 0) cs = slotF[s];                       // previous segment, rank P-1 (R-4)
                     else if (Pc[q]) cs = slotF[s - j * K];          // producer join slot (R-5)
                     else cs = ZS;
                     if (k + 1 < K) ps = slotF[s + 1];
-                    else if (Cc[q] == 0) { ps = nF + slotB[s]; ex |= E_TURN; }   // loss turnaround (R-6)
+                    else if (Cc[q] == 0) { ps = nF + slotB[s]; ex = (ex & ~(3u << 24)) | E_SMINUS; }   // loss turnaround (R-6)
                     else {
                         uint32_t cmods = 0, c1 = 0;
                         for (uint32_t c = 0; c < nmod; c++)
@@ -283,12 +301,12 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 const bool pres = j < Mb[q];
                 if (slotF[s] != 0xFFFFu) {
                     uint64_t f0 = 0;
-                    if (pres) f0 = (k > 0 ? 1ull : (uint64_t)Pc[q]) << PEND_SHIFT;
+                    if (pres) f0 = (uint64_t)((256u - (k > 0 ? 1u : Pc[q])) & 0xFFu) << PEND_SHIFT;
                     depAll[slotF[s]] = f0;
                 }
                 if (slotB[s] != 0xFFFFu) {
                     uint64_t bp = 0;
-                    if (pres) bp = ((k < Km1 || Cc[q] == 0) ? 1ull : (uint64_t)Cc[q]) << PEND_SHIFT;
+                    if (pres) bp = (uint64_t)((256u - ((k < Km1 || Cc[q] == 0) ? 1u : Cc[q])) & 0xFFu) << PEND_SHIFT;
                     depAll[nF + slotB[s]] = bp;
                 }
             }
@@ -334,7 +352,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             const uint32_t w = (wrapC && !d) ? 0u : T.w;   // rank 0's F wrap slot already holds + p2p
             uint64_t dep = (v + w) & VAL_MASK;
             if (ready && !wrapC && idx + D < nb)   // evicted from the channel ring: exact spill copy
-                dep = spill[(d ? (P + r + 1) : (r - 1)) * n_max + idx] + w;
+                dep = spill_load(spill, d, r, P, n_max, idx) + w;
 
             const uint32_t prog = __ballot_sync(FULL, ready);
             const uint32_t alive = __ballot_sync(FULL, !done);
@@ -353,17 +371,15 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 busy += lat;
                 cur = d ? cur - act : cur + act;
                 peak = cur > peak ? cur : peak;
-                // wrap publish value: F -> end + p2p (chain / join), or end - p2p for the loss turnaround
-                // (its B consumer adds p2p back); B -> end
-                const int64_t pw = d ? 0 : ((e.x & E_TURN) ? -(int64_t)T.w : (int64_t)T.w);
-                const uint64_t pv = (end + (uint64_t)pw) & VAL_MASK;
-                const uint64_t ov = pold & VAL_MASK;
-                const uint64_t rmw = (pv > ov ? pv : ov) | ((pold & ~VAL_MASK) - (1ull << PEND_SHIFT));
+                const int32_t sgn = (int32_t)(e.x << 6) >> 30;                 // publish factor -1 / 0 / +1
+                const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
+                const uint64_t cand = (pold & HIGH_MASK) | pv;
+                const uint64_t rmw = (cand > pold ? cand : pold) + (1ull << PEND_SHIFT);
                 *pa = wrapP ? rmw : end;
                 if (!wrapP) {
                     const uint32_t cc = ((d ? up : dn) >> sh) & 0xFFFFu;   // consumer neighbour's count
-                    if (idx >= D && cc + D <= idx)        // consumer is >= D behind: keep the old entry
-                        spill[(d ? (P + r) : r) * n_max + idx - D] = pold;
+                    if (idx >= cc + D)                    // consumer is >= D behind: keep the old entry
+                        spill_keep(spill, d, r, P, n_max, idx, pold);
                 } else if (e.x & E_MULTI) {               // several join targets (rare); the plain store hit SINK
                     const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
                     const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
@@ -371,8 +387,8 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                     for (uint32_t c = 0; c < nmod; c++) {
                         if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
                         uint64_t *sl = &depAll[d ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
-                        const uint64_t old = *sl, o2 = old & VAL_MASK;
-                        *sl = (pv > o2 ? pv : o2) | ((old & ~VAL_MASK) - (1ull << PEND_SHIFT));
+                        const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
+                        *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
                     }
                 }
                 cnt += 1u << sh;
