@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         uint32_t t = 0, cnt = 0;                 // cnt = fi | bi << 16
         uint64_t tlast = 0, busy = 0;
         uint32_t cur = 0, peak = 0;
+        const uint32_t *wptr = reinterpret_cast<const uint32_t *>(rec + kp.off_fb) + 2 * P + r;   // word 2 of this row
         const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
         const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
         const uint32_t wrapBits = (isFirst ? 1u : 0u) | (isLast ? 2u : 0u);   // bit d: consumes dir d via wrap
@@ -393,10 +394,10 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 }
                 cnt += 1u << sh;
                 t++;
-                if ((t & 31) == 0) {
+                if ((t & 31) == 0) {                      // next 32 F/B bits: the word after next is prefetched
                     wcur = wnext;
-                    const uint32_t nw = (t >> 5) + 1;
-                    if (nw < kp.fbw) wnext = ldg32(rec + kp.off_fb + 4 * (nw * P + r));
+                    if (t + 32 < S2) wnext = __ldg(wptr);
+                    wptr += P;
                 }
                 done = t == S2;
             }
