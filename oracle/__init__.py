@@ -61,6 +61,9 @@ def _load():
         lib.oracle_timeline.restype = ctypes.c_int
         lib.oracle_timeline.argtypes = [ctypes.POINTER(_OProblem), ctypes.POINTER(_OCands), ctypes.c_uint64,
                                         ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_interleave.restype = ctypes.c_int
+        lib.oracle_interleave.argtypes = [ctypes.POINTER(_OProblem), ctypes.POINTER(_OCands), ctypes.c_uint64,
+                                          ctypes.c_uint64] + [ctypes.c_void_p] * 7 + [ctypes.c_int]
         lib.oracle_argmin.restype = ctypes.c_int64
         lib.oracle_argmin.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
         _lib = lib
@@ -123,6 +126,25 @@ def evaluate(pb, cands, first: int = 0, count: Optional[int] = None, threads: in
                     res.status.ctypes.data, res.oom_mask.ctypes.data, res.bubble.ctypes.data,
                     res.peaks.ctypes.data, res.busy.ctypes.data, threads)
     return res
+
+
+def interleave(pb, cands, first: int = 0, count: Optional[int] = None, threads: int = 1):
+    """I1-I6: DIP's dual-queue greedy interleaving of each candidate's split and
+    forward / backward priority orders (its F/B bits are ignored). Returns (bits, Results):
+    bits [count, P, fbw] in the host-view layout, and the score of the built schedule."""
+    for nme in ("split", "n", "fwd", "bwd", "fb"):
+        assert getattr(cands, nme).flags["C_CONTIGUOUS"], nme
+    if count is None:
+        count = cands.count - first
+    lib = _load()
+    bd = _Bound(pb, cands)
+    res = Results(count, pb.P)
+    bits = np.zeros((count, pb.P, pb.fbw), np.uint32)
+    rc = lib.oracle_interleave(ctypes.byref(bd.pb), ctypes.byref(bd.cs), first, count, bits.ctypes.data,
+                               res.makespan.ctypes.data, res.status.ctypes.data, res.oom_mask.ctypes.data,
+                               res.bubble.ctypes.data, res.peaks.ctypes.data, res.busy.ctypes.data, threads)
+    assert rc == 0
+    return bits, res
 
 
 def timeline(pb, cands, x: int):

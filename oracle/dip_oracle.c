@@ -19,6 +19,7 @@
  *   O9  memory timeline    P:703-705 "tensor lifetimes ... peak memory usage" (R-9, R-10)
  *   O10 outputs            P:499 score = "end-to-end iteration time"; bubble P:248 (R-16)
  *   O11 argmin             P:499-501 best score; ties -> lowest index (R-14, R-15)
+ *   I1-I6 interleaving     P:511-548 the dual-queue greedy, see below
  *
  * Integers everywhere (ns, KiB); u64 accumulators.  The only floating-point
  * value, the bubble ratio, is one IEEE double division of two exact integers.
@@ -355,6 +356,263 @@ int oracle_timeline(const oproblem *pb, const ocands *cs, uint64_t x, uint64_t *
     ores r;
     eval_one(pb, cs, x, &r, NULL, tl_start, tl_end);
     return (int)r.status;
+}
+
+/* ======================================================================================
+ * I1-I6: DIP's greedy dual-queue stage interleaving (§5.2), the row f1 of
+ * given a split and segment priorities (the forward and backward priority orders
+ * = fwd_seq / bwd_seq of a candidate; its F/B bits are ignored), build every rank's F/B
+ * interleaving and its timing. Readings: in-order queues (each rank's Q_fw / Q_bw
+ * head is its next segment in priority order, R-26/A.8); a head's t_start is finite once all its
+ * predecessors are placed; rank = argmin t_min, ties to the lowest rank;
+ * step 3 "both t_fw < t_last and t_bw < t_last" strict, alternating on the last type;
+ * step 4 smallest t_start, ties to the backward (R-29); memory gating: the forward
+ * queue is disabled while placing its head would exceed the rank's budget (R-30); if every rank
+ * is blocked only by gating, the gate is lifted for one step (R-31), the overflow shows as OOM.
+ * ====================================================================================== */
+typedef struct { uint64_t end; uint8_t placed; } inode;
+
+static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uint32_t *bits_out /* [P][fbw] */,
+                           ores *res, uint64_t *peaks) {
+    const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
+    const uint32_t n_max = cs->n_max, fbw = cs->fbw;
+    const uint8_t *split = cs->split + x * (uint64_t)m * nm;
+    const uint16_t *fwd = cs->fwd + x * (uint64_t)n_max;
+    const uint16_t *bwd = cs->bwd + x * (uint64_t)n_max;
+    const uint32_t ncand = cs->n[x];
+    res->makespan = UINT64_MAX; res->busy = 0; res->status = ST_BAD; res->oom_mask = 0; res->bubble = -1.0;
+    for (uint32_t r = 0; r < P; r++) { if (peaks) peaks[r] = 0; }
+    memset(bits_out, 0, sizeof(uint32_t) * P * fbw);
+
+    /* I1 (= O1-O4 without the bit strings): segment ids, split, work units, sequences */
+    uint32_t idmax = seg_count_max(pb);
+    uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
+    uint32_t *W = calloc(idmax + 1, sizeof(uint32_t));
+    uint8_t *present = calloc(idmax + 1, 1);
+    uint32_t *sb = malloc(sizeof(uint32_t) * (idmax + 1)), *si = malloc(sizeof(uint32_t) * (idmax + 1));
+    uint32_t *sj = malloc(sizeof(uint32_t) * (idmax + 1)), *sk = malloc(sizeof(uint32_t) * (idmax + 1));
+    int bad = 0;
+    uint32_t acc = 0, n = 0;
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            base[b * nm + i] = acc;
+            for (uint32_t j = 0; j < pb->max_split[i]; j++)
+                for (uint32_t k = 0; k < pb->K[i]; k++) {
+                    uint32_t id = acc + j * pb->K[i] + k;
+                    sb[id] = b; si[id] = i; sj[id] = j; sk[id] = k;
+                }
+            acc += pb->max_split[i] * pb->K[i];
+        }
+    for (uint32_t b = 0; b < m && !bad; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            uint32_t q = b * nm + i;
+            uint32_t lo = pb->inst_off[q], N = pb->inst_off[q + 1] - lo, M = split[q];
+            uint32_t cap = N < pb->max_split[i] ? N : pb->max_split[i];
+            if ((N == 0) != (M == 0) || M > cap) { bad = 1; break; }
+            if (M == 0) continue;
+            uint32_t st[16];
+            oracle_split(N, M, st);
+            for (uint32_t j = 0; j < M; j++) {
+                uint32_t w = 0;
+                for (uint32_t u = st[j]; u < st[j + 1]; u++) w += pb->inst_units[lo + u];
+                for (uint32_t k = 0; k < pb->K[i]; k++) {
+                    uint32_t id = base[q] + j * pb->K[i] + k;
+                    present[id] = 1; W[id] = w; n++;
+                }
+            }
+        }
+    if (!bad && (ncand != n || n > n_max)) bad = 1;
+    if (!bad) {
+        uint8_t *seenF = calloc(idmax + 1, 1), *seenB = calloc(idmax + 1, 1);
+        for (uint32_t p = 0; p < n_max && !bad; p++) {
+            if (p < n) {
+                uint32_t a = fwd[p], c = bwd[p];
+                if (a >= idmax || c >= idmax || !present[a] || !present[c] || seenF[a] || seenB[c]) bad = 1;
+                else { seenF[a] = 1; seenB[c] = 1; }
+            } else if (fwd[p] != 0xFFFF || bwd[p] != 0xFFFF) bad = 1;
+        }
+        free(seenF); free(seenB);
+    }
+    if (bad) goto done;
+    if (n == 0) { res->makespan = 0; res->status = ST_OK; res->bubble = 0.0; goto done; }
+    {
+        /* node (dir, s, r) -> index (r * 2 + dir) * idmax + s */
+        const uint32_t NN = P * 2 * idmax;
+        inode *nd = calloc(NN, sizeof(inode));
+#define NODE(dir, s, r) (((r) * 2u + (dir)) * idmax + (s))
+        uint32_t *fi = calloc(P, sizeof(uint32_t)), *bi = calloc(P, sizeof(uint32_t));
+        uint64_t *tlast = calloc(P, sizeof(uint64_t)), *cur = calloc(P, sizeof(uint64_t)), *pk = calloc(P, sizeof(uint64_t));
+        int *last = malloc(sizeof(int) * P);
+        for (uint32_t r = 0; r < P; r++) last[r] = -1;
+        uint64_t mk = 0, busy = 0;
+        int dead = 0;
+        /* I2: stage costs (as O6) */
+#define LAYERS(i, k, r) ((uint64_t)layers_of(pb, (i), (k) * P + (r)))
+#define LAT(dir, s, r) (LAYERS(si[s], sk[s], r) * (uint64_t)((dir) ? pb->tab_b[pb->tab_off[si[s]] + W[s]] : pb->tab_f[pb->tab_off[si[s]] + W[s]]))
+#define ACT(s, r) (LAYERS(si[s], sk[s], r) * (uint64_t)pb->tab_act[pb->tab_off[si[s]] + W[s]])
+#define P2P(s) ((uint64_t)pb->tab_p2p[pb->tab_off[si[s]] + W[s]])
+        for (uint32_t step = 0; step < P * 2 * n; step++) {
+            /* I3: per rank, the t_start of both queue heads (UINT64_MAX = not ready / empty) */
+            uint64_t tf[32], tb[32];
+            int gated[32];
+            for (uint32_t r = 0; r < P; r++) {
+                for (int dir = 0; dir < 2; dir++) {
+                    uint32_t h = dir ? bi[r] : fi[r];
+                    uint64_t ts = UINT64_MAX;
+                    if (h < n) {
+                        uint32_t s = dir ? bwd[h] : fwd[h];
+                        uint32_t b = sb[s], i = si[s], k = sk[s], K = pb->K[i];
+                        int ok = 1;
+                        uint64_t t0 = 0;
+                        /* cross-rank predecessors, exactly the edges of O7 (the rank order is what
+                         * this algorithm decides, so there is no same-rank chain edge here) */
+#define DEP(nid, wgt) do { inode *pn = &nd[nid]; if (!pn->placed) ok = 0; else if (pn->end + (wgt) > t0) t0 = pn->end + (wgt); } while (0)
+                        if (dir == 0) {
+                            if (r > 0) DEP(NODE(0, s, r - 1), P2P(s));
+                            else if (k > 0) DEP(NODE(0, s - 1, P - 1), P > 1 ? P2P(s - 1) : 0);
+                            else for (uint32_t ip = 0; ip < nm; ip++) {
+                                if (!((pb->producer_mask[i] >> ip) & 1u)) continue;
+                                for (uint32_t jp = 0; jp < split[b * nm + ip]; jp++) {
+                                    uint32_t pr = base[b * nm + ip] + jp * pb->K[ip] + pb->K[ip] - 1;
+                                    DEP(NODE(0, pr, P - 1), P > 1 ? P2P(pr) : 0);
+                                }
+                            }
+                        } else {
+                            if (r + 1 < P) DEP(NODE(1, s, r + 1), P2P(s));
+                            else if (k + 1 < K) DEP(NODE(1, s + 1, 0), P > 1 ? P2P(s) : 0);
+                            else {
+                                int any = 0;
+                                for (uint32_t ic = 0; ic < nm; ic++) {
+                                    if (!((pb->producer_mask[ic] >> i) & 1u)) continue;
+                                    for (uint32_t jc = 0; jc < split[b * nm + ic]; jc++) {
+                                        DEP(NODE(1, base[b * nm + ic] + jc * pb->K[ic], 0), P > 1 ? P2P(s) : 0);
+                                        any = 1;
+                                    }
+                                }
+                                if (!any) DEP(NODE(0, s, P - 1), 0);
+                            }
+                        }
+#undef DEP
+                        if (ok) ts = t0;
+                    }
+                    if (dir) tb[r] = ts; else tf[r] = ts;
+                }
+                /* I4: memory gating: the forward queue is disabled while placing its
+                 * head would exceed the rank's budget (R-30) */
+                gated[r] = 0;
+                if (tf[r] != UINT64_MAX && cur[r] + ACT(fwd[fi[r]], r) > pb->budget_kib[r]) gated[r] = 1;
+            }
+            /* I5: the rank with the smallest t_min, ties to the lowest rank */
+            int rr = -1, relax = 0;
+            uint64_t best = UINT64_MAX;
+            for (uint32_t r = 0; r < P; r++) {
+                uint64_t f = gated[r] ? UINT64_MAX : tf[r];
+                uint64_t tm = f < tb[r] ? f : tb[r];
+                if (tm < best) { best = tm; rr = (int)r; }
+            }
+            if (rr < 0) {   /* every rank blocked by the gate only: lift it for one step (R-31) */
+                for (uint32_t r = 0; r < P; r++) {
+                    uint64_t tm = tf[r] < tb[r] ? tf[r] : tb[r];
+                    if (tm < best) { best = tm; rr = (int)r; }
+                }
+                relax = 1;
+            }
+            if (rr < 0) { dead = 1; break; }
+            const uint32_t r = (uint32_t)rr;
+            const uint64_t f = (gated[r] && !relax) ? UINT64_MAX : tf[r], bb = tb[r];
+            /* I6: steps 2-4 */
+            int dir;
+            if (f != UINT64_MAX && bb != UINT64_MAX && f < tlast[r] && bb < tlast[r])
+                dir = last[r] == 0 ? 1 : 0;                 /* emulate 1F1B: alternate */
+            else if (f == UINT64_MAX) dir = 1;
+            else if (bb == UINT64_MAX) dir = 0;
+            else dir = bb <= f ? 1 : 0;                     /* smallest t_start; ties -> backward (R-29) */
+            uint32_t h = dir ? bi[r] : fi[r];
+            uint32_t s = dir ? bwd[h] : fwd[h];
+            uint64_t ts = dir ? bb : f;
+            uint64_t st = ts > tlast[r] ? ts : tlast[r];
+            uint64_t lat = LAT(dir, s, r);
+            uint64_t en = st + lat;
+            nd[NODE(dir, s, r)].end = en;
+            nd[NODE(dir, s, r)].placed = 1;
+            tlast[r] = en;
+            last[r] = dir;
+            busy += lat;
+            if (en > mk) mk = en;
+            uint32_t t = fi[r] + bi[r];
+            if (dir) { bits_out[r * fbw + t / 32] |= 1u << (t % 32); bi[r]++; cur[r] -= ACT(s, r); }
+            else { fi[r]++; cur[r] += ACT(s, r); if (cur[r] > pk[r]) pk[r] = cur[r]; }
+        }
+        uint32_t oom = 0;
+        for (uint32_t r = 0; r < P; r++) {
+            if (peaks) peaks[r] = pk[r];
+            if (pk[r] > pb->budget_kib[r]) oom |= 1u << r;
+        }
+        res->oom_mask = oom;
+        if (dead) {
+            res->status = ST_DEADLOCK;
+        } else {
+            res->makespan = mk;
+            res->busy = busy;
+            uint64_t den = (uint64_t)P * mk;
+            res->bubble = den ? (double)(den - busy) / (double)den : 0.0;
+            res->status = oom ? ST_OOM : ST_OK;
+        }
+#undef LAYERS
+#undef LAT
+#undef ACT
+#undef P2P
+#undef NODE
+        free(nd); free(fi); free(bi); free(tlast); free(cur); free(pk); free(last);
+    }
+done:
+    free(base); free(W); free(present); free(sb); free(si); free(sj); free(sk);
+}
+
+typedef struct {
+    const oproblem *pb;
+    const ocands *cs;
+    uint64_t lo, hi, first;
+    uint32_t *bits;
+    uint64_t *makespan, *busy, *peaks;
+    uint32_t *status, *oom;
+    double *bubble;
+} ijob_t;
+
+static void *iworker(void *arg) {
+    ijob_t *j = (ijob_t *)arg;
+    const uint32_t P = j->pb->P, fbw = j->cs->fbw;
+    for (uint64_t x = j->lo; x < j->hi; x++) {
+        ores r;
+        uint64_t o = x - j->first;
+        interleave_one(j->pb, j->cs, x, j->bits + o * P * fbw, &r, j->peaks ? j->peaks + o * P : NULL);
+        j->makespan[o] = r.makespan; j->busy[o] = r.busy; j->status[o] = r.status;
+        j->oom[o] = r.oom_mask; j->bubble[o] = r.bubble;
+    }
+    return NULL;
+}
+
+/* Interleave candidates [first, first+count): writes each one's F/B bits ([count][P][fbw]) and
+ * the resulting schedule's score (as oracle_eval). */
+int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint64_t count, uint32_t *bits,
+                      uint64_t *makespan, uint32_t *status, uint32_t *oom_mask, double *bubble, uint64_t *peaks,
+                      uint64_t *busy, int threads) {
+    if (pb->P > 32) return -1;
+    if (threads < 1) threads = 1;
+    if (threads > 512) threads = 512;
+    if ((uint64_t)threads > count) threads = count ? (int)count : 1;
+    pthread_t th[512];
+    ijob_t jobs[512];
+    uint64_t per = (count + threads - 1) / threads;
+    for (int t = 0; t < threads; t++) {
+        uint64_t lo = first + per * t, hi = lo + per;
+        if (hi > first + count) hi = first + count;
+        if (lo > hi) lo = hi;
+        jobs[t] = (ijob_t){pb, cs, lo, hi, first, bits, makespan, busy, peaks, status, oom_mask, bubble};
+        pthread_create(&th[t], NULL, iworker, &jobs[t]);
+    }
+    for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+    return 0;
 }
 
 /* O11: lowest index among status OK with minimal makespan; returns -1 if none. */

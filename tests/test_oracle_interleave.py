@@ -1,0 +1,98 @@
+"""Pins of the oracle's dual-queue interleaving (I1-I6, §5.2).
+
+Expected values: the 1F1B closed form, SURVEY App. A.8's exact-order and peak results (derived
+there independently of this code), and the replay identity: the greedy places every stage at
+max(t_last, t_start), so re-timing its output orders with the fixed-order simulator (O1-O10, pinned
+in test_oracle_pins.py) must reproduce its makespan, peaks and bubble exactly.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests import helpers as H
+
+OK, OOM, DL, BAD = oracle.ST_OK, oracle.ST_OOM, oracle.ST_DEADLOCK, oracle.ST_BAD
+
+
+@pytest.mark.parametrize("tf,tb", [(1, 1), (1, 2), (2, 3)])
+def test_ungated_makespan_equals_1f1b(tf, tb):
+    # App. A.8: ungated, homogeneous single module -> the 1F1B makespan (m+P-1)(t_f+t_b)
+    for P in range(1, 7):
+        for m in range(1, 9):
+            pb = H.uniform_problem(P, m, tf, tb, act=1)
+            cs = H.candidates_from_orders(pb, [[1] * m], [H.one_f_one_b(P, m)])
+            bits, r = oracle.interleave(pb, cs)
+            assert int(r.makespan[0]) == (m + P - 1) * (tf + tb), (P, m)
+
+
+def test_ungated_front_loads_forwards():
+    # App. A.8: P=8, m=16 (t_f=1, t_b=2) ungated, strict "<" in step 3 (R-26): peaks
+    # [16,16,16,15,14,10,6,2] instead of 1F1B's [8,7,...,1] -- the reason for memory gating
+    pb = H.uniform_problem(8, 16, 1, 2, act=1)
+    cs = H.candidates_from_orders(pb, [[1] * 16], [H.one_f_one_b(8, 16)])
+    bits, r = oracle.interleave(pb, cs)
+    assert r.peaks[0].tolist() == [16, 16, 16, 15, 14, 10, 6, 2]
+    assert int(r.makespan[0]) == (16 + 8 - 1) * 3
+
+
+@pytest.mark.parametrize("tf,tb", [(1, 1), (1, 2), (2, 3)])
+def test_gated_reproduces_exact_1f1b_orders(tf, tb):
+    # App. A.8: with capacity (P - r) activations per rank, the gated greedy emits exactly Megatron's
+    # 1F1B per-rank orders (R-17) for every P <= 8, m <= 16
+    for P in range(1, 9):
+        for m in range(1, 17):
+            pb = H.uniform_problem(P, m, tf, tb, act=3, budget=[(P - r) * 3 for r in range(P)])
+            ref = H.candidates_from_orders(pb, [[1] * m], [H.one_f_one_b(P, m)])
+            bits, r = oracle.interleave(pb, ref)
+            assert np.array_equal(bits[0], ref.fb[0]), (P, m)
+            assert r.status[0] == OK and r.peaks[0].tolist() == [min(P - k, m) * 3 for k in range(P)]
+
+
+def _replay(pb, cs, bits):
+    c2 = cs.subset(np.arange(cs.count))
+    c2.fb[:] = bits
+    return oracle.evaluate(pb, c2, threads=8)
+
+
+@pytest.mark.parametrize("name,count", [("toy", 256), ("12B", 96), ("37B", 48), ("T2V", 32), ("94B", 8)])
+def test_replay_identity_on_generated(name, count):
+    # the greedy's own times == the longest-path replay of the orders it emits (App. A.8)
+    pb = gen.make_problem(name)
+    cs = gen.generate(pb, 0, count, mode=1 if name == "toy" else 0, p_mutate=0.0, p_bad=0.0)
+    bits, r = oracle.interleave(pb, cs, threads=8)
+    rp = _replay(pb, cs, bits)
+    assert (r.status != DL).all()
+    for k in ("status", "makespan", "oom_mask", "peaks", "busy"):
+        assert np.array_equal(getattr(r, k), getattr(rp, k)), k
+    assert np.array_equal(r.bubble.view(np.uint64), rp.bubble.view(np.uint64))
+    # every rank runs each segment exactly once: n forward and n backward slots per rank
+    for x in range(count):
+        n = int(cs.n[x])
+        ones = [sum(bin(int(w)).count("1") for w in bits[x, q]) for q in range(pb.P)]
+        assert ones == [n] * pb.P
+
+
+def test_gating_respects_budget_when_feasible():
+    # with a budget of one forward activation per rank beyond the 1F1B minimum, no rank exceeds it
+    pb = gen.make_problem("12B")
+    cs = gen.generate(pb, 0, 64, p_mutate=0.0, p_bad=0.0)
+    bits, r = oracle.interleave(pb, cs, threads=8)
+    ok = r.status == OK
+    assert ok.any()
+    assert (r.peaks[ok] <= pb.budget_kib[None, :].astype(np.uint64)).all()
+
+
+def test_bad_and_deadlocked_priority_orders():
+    pb = H.uniform_problem(2, 2, 1, 2)
+    cs = H.candidates_from_orders(pb, [[1, 1]], [H.one_f_one_b(2, 2)])
+    c = cs.subset([0])
+    c.fwd[0, 1] = c.fwd[0, 0]                 # duplicate id -> BAD_ENCODING (R-11)
+    bits, r = oracle.interleave(pb, c)
+    assert r.status[0] == BAD and int(r.makespan[0]) == 2 ** 64 - 1
+    # a forward order that is not a linear extension of the segment DAG (k=1 before k=0) deadlocks
+    pb2 = H.uniform_problem(2, 1, 1, 2, K=2)
+    c2 = H.candidates_from_orders(pb2, [[1]], [[[("F", 0), ("F", 1), ("B", 1), ("B", 0)]] * 2])
+    c2.fwd[0, :2] = [1, 0]
+    bits, r = oracle.interleave(pb2, c2)
+    assert r.status[0] == DL
