@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--host-chunk", type=int, default=65536)
+    ap.add_argument("--f1-count", type=int, default=65536,
+                    help="candidates for the f1 (dual-queue interleaving) measurement; 0 disables it")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -271,6 +273,38 @@ def main():
                "h2d_bytes_per_step": per * model.stride, "d2h_bytes_per_step": 8,
                "path": "dip_eval_host: pinned host records, 64K-record chunks, H2D overlapped with scoring"}
 
+    # ---- DIP's dual-queue interleaving on the first f1-count records
+    f1 = None
+    if args.f1_count > 0:
+        cnt = min(per, args.f1_count)
+        d_f1 = d_rec[: cnt * model.stride].clone()
+        r_f1 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(args.steps, 5))
+        a.record(stream)
+        for _ in range(reps):
+            dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tf1 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tf1, op=dist.ReduceOp.MAX)
+        f1 = {"what": "dip_interleave: build each candidate's F/B interleaving with the paper's dual-queue "
+                      "greedy (P:511-548) from its split + priority orders, then score it",
+              "value": cnt * world * reps / (float(tf1[0]) / 1e3), "unit": "candidates/s",
+              "candidates_per_gpu": cnt, "ms_per_call": float(tf1[0]) / reps}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            import oracle
+            sub = cs.subset(np.arange(min(cnt, 2048)))
+            t0 = time.perf_counter()
+            oracle.interleave(pb, sub, threads=os.cpu_count() or 1)
+            f1["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
+                                "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
+        del d_f1, r_f1
+
     hbm_peak, sm_max, src = peaks()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -302,7 +336,7 @@ def main():
             "hbm": {"achieved": bytes_launch / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bytes_launch / kern_s / 1e9 / hbm_peak,
                     "algorithmic": "record + 24 B result + 4P B peaks per candidate", "peak_source": src},
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks, "f1_interleave": f1,
             "status_hist": {"ok": hist[0], "oom": hist[1], "deadlock": hist[2], "bad_encoding": hist[3]},
             "winner": {"found": win.found, "global_index": win.global_index, "makespan_ns": win.makespan_ns},
             "setup_s": {"generate": round(t_gen, 1)},

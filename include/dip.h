@@ -149,6 +149,18 @@ dip_status dip_workspace_free(dip_workspace *w);
 dip_status dip_eval_schedules(const dip_model *m, dip_workspace *w, const void *d_records, size_t count,
                               dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
 
+/* DIP's greedy dual-queue stage interleaving (§5.2):
+ * for every record, take its split and its forward / backward segment orders as the priority
+ * orders of the per-rank queues, build each rank's F/B interleaving with the paper's iterative
+ * scheduling (rank with the smallest t_min, 1F1B alternation when both heads are ready before
+ * t_last, else the smaller t_start; forward queue disabled while the next forward would exceed
+ * the rank's budget), and score the result. The records' F/B bit rows are OVERWRITTEN in place
+ * with the built interleaving (zero for BAD_ENCODING; a DEADLOCK keeps the partial rows), so
+ * dip_eval_schedules on the same records reproduces d_results exactly. The fused argmin key is
+ * updated as by dip_eval_schedules (dip_argmin works after it). Asynchronous on `stream`. */
+dip_status dip_interleave(const dip_model *m, dip_workspace *w, void *d_records, size_t count,
+                          dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+
 typedef struct {
     int32_t found;            /* 0 if no candidate has status OK on any rank */
     int32_t rank;             /* owning rank */

@@ -454,9 +454,10 @@ dip_status dip_workspace_free(dip_workspace *w) {
 // ---------------------------------------------------------------- eval -----------------
 static dip_status launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                                uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
-                               uint32_t *d_peaks, cudaStream_t s) {
+                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out = nullptr) {
     KParams kp = M->kp;
     kp.records = static_cast<const uint8_t *>(d_records);
+    kp.records_out = records_out;
     kp.count = count;
     kp.index_base = index_base;
     kp.results = d_results;
@@ -492,6 +493,23 @@ dip_status dip_eval_schedules(const dip_model *M, dip_workspace *w, const void *
     w->last_fused = fused;
     if (!count) return DIP_OK;
     return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s);
+}
+
+dip_status dip_interleave(const dip_model *M, dip_workspace *w, void *d_records, size_t count, dip_result *d_results,
+                          uint32_t *d_peaks, void *stream) {
+    if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
+    if (count && (!d_records || !d_results)) return fail(DIP_EINVAL, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t idx_bits = bits_for(std::max<uint64_t>(count, 2));
+    const bool fused = fused_ok(M, idx_bits);
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
+    w->last_results = d_results;
+    w->last_count = count;
+    w->last_idx_bits = idx_bits;
+    w->last_fused = fused;
+    if (!count) return DIP_OK;
+    return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s,
+                        static_cast<uint8_t *>(d_records));
 }
 
 // local winner -> (makespan, local index) on the host; exact two-pass scan when not fused

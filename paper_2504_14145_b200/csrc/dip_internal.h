@@ -37,6 +37,7 @@ struct KParams {
     uint32_t warps_per_block, cpg;
     // per launch
     const uint8_t *records;
+    uint8_t *records_out;       // non-null: interleave mode (f1) writes the F/B bit rows here
     uint64_t count, index_base;
     dip_result *results;
     uint32_t *peaks;

@@ -65,6 +65,15 @@ __device__ __forceinline__ uint64_t group_max(uint64_t v) {
     return v;
 }
 template <int G>
+__device__ __forceinline__ uint64_t group_min(uint64_t v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o, G);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+template <int G>
 __device__ __forceinline__ uint64_t group_sum(uint64_t v) {
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
@@ -101,7 +110,7 @@ __device__ __noinline__ void spill_keep(unsigned long long *spill, uint32_t d, u
     spill[(d ? (P + r) : r) * n_max + idx - RING_D] = v;
 }
 
-template <int G>
+template <int G, int MODE>   // MODE 0: score the given schedules; MODE 1: build them (f1) and score
 __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t blob_bar;
@@ -226,7 +235,11 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         }
         // F/B bit rows: exactly n ones in [0, 2n), zeros beyond
         uint32_t wcur = 0, wnext = 0;
-        if (laneOn) {
+        if (MODE == 1 && laneOn && gvalid) {   // the interleaving overwrites the record's F/B bit rows
+            uint32_t *fbo = reinterpret_cast<uint32_t *>(kp.records_out + cand * (uint64_t)kp.stride + kp.off_fb);
+            for (uint32_t w = 0; w < kp.fbw; w++) fbo[w * P + r] = 0u;
+        }
+        if (MODE == 0 && laneOn) {
             const uint32_t lim = 2 * n;
             uint32_t ones = 0;
             for (uint32_t w = 0; w < kp.fbw; w++) {
@@ -314,6 +327,11 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         }
         __syncwarp();
 
+        bool dl = false;
+        uint64_t tlast = 0, busy = 0;
+        uint32_t cur = 0, peak = 0;
+        const uint32_t S2 = 2 * n;
+        if (MODE == 0) {
         // ---------------- K3: lock-step wavefront longest path ----------------
         // Per round every lane of the group tries its next slot (F if bit t is 0, else B):
         // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
@@ -321,12 +339,8 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         // end into its own channel ring (or read-modify-write a wrap slot). The F and B state is
         // indexed by isB with shifts (counts packed as fi | bi << 16) rather than selects.
         // Channel rings are [2][D][P] u64 (F rings, then B rings; lane x owns column x).
-        const uint32_t S2 = 2 * n;
         bool done = bad || !laneOn || n == 0;
-        bool dl = false;
         uint32_t t = 0, cnt = 0;                 // cnt = fi | bi << 16
-        uint64_t tlast = 0, busy = 0;
-        uint32_t cur = 0, peak = 0;
         const uint32_t *wptr = reinterpret_cast<const uint32_t *>(rec + kp.off_fb) + 2 * P + r;   // word 2 of this row
         const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
         const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
@@ -417,6 +431,123 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
         }
 
+        } else {
+        // ---------------- f1: DIP's dual-queue greedy interleaving ----------------
+        // One stage per step per candidate, exactly in the order of the sequential algorithm: every
+        // lane (rank) evaluates the t_start of its two in-order queue heads (the dependency values
+        // come through the same channel rings and wrap slots as the scorer), applies the memory
+        // gate (R-30), the group picks the rank with the smallest t_min (ties to the
+        // lowest rank) and that rank places one stage: alternating F/B when both heads are
+        // ready before t_last, else the smaller t_start (ties to B, R-29). If every rank
+        // is blocked by its gate only, the gate is lifted for one step (R-31).
+        uint32_t cnt = 0, wbuf = 0;
+        int last = -1;
+        bool done = bad || !laneOn || n == 0;
+        uint32_t *fbOut = reinterpret_cast<uint32_t *>(kp.records_out + (gvalid ? cand : 0) * (uint64_t)kp.stride + kp.off_fb) + r;
+        const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
+        const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
+        const uint32_t bud = budget[laneOn ? r : 0];
+        for (;;) {
+            const uint32_t up = __shfl_up_sync(FULL, cnt, 1, G);
+            const uint32_t dn = __shfl_down_sync(FULL, cnt, 1, G);
+            const uint32_t fi = cnt & 0xFFFFu, bi = cnt >> 16;
+            const bool hasF = !done && fi < n, hasB = !done && bi < n;
+            // forward head
+            const uint2 eF = hasF ? posAll[fi] : make_uint2(0u, 0u);
+            const uint4 TF = tab[eF.x & 0xFFFu];
+            const uint32_t layF = layers[((eF.x >> 12) & 0xFFFu) + r];
+            const uint32_t nbF = up & 0xFFFFu;
+            uint64_t vF = hasF ? (isFirst ? depAll[eF.y & 0xFFFFu] : ringAll[(fi & (D - 1)) * P + colIn0]) : 0ull;
+            const bool rdyF = hasF && (isFirst ? (vF >> PEND_SHIFT) == 0 : nbF > fi);
+            if (rdyF && !isFirst && fi + D < nbF) vF = spill_load(spill, 0, r, P, n_max, fi);
+            const uint64_t tF = (vF + (isFirst ? 0u : TF.w)) & VAL_MASK;
+            // backward head
+            const uint2 eB = hasB ? posAll[n_max + bi] : make_uint2(0u, 0u);
+            const uint4 TB = tab[eB.x & 0xFFFu];
+            const uint32_t layB = layers[((eB.x >> 12) & 0xFFFu) + r];
+            const uint32_t nbB = dn >> 16;
+            uint64_t vB = hasB ? (isLast ? depAll[eB.y & 0xFFFFu] : ringAll[(bi & (D - 1)) * P + colIn1]) : 0ull;
+            const bool rdyB = hasB && (isLast ? (vB >> PEND_SHIFT) == 0 : nbB > bi);
+            if (rdyB && !isLast && bi + D < nbB) vB = spill_load(spill, 1, r, P, n_max, bi);
+            const uint64_t tB = (vB + TB.w) & VAL_MASK;
+            // memory gate and the group's argmin of (t_min, rank)
+            const uint32_t actF = layF * TF.z;
+            const bool gated = rdyF && cur + actF > bud;
+            const uint64_t INF = ~0ull;
+            const uint64_t kF = (rdyF && !gated) ? tF : INF, kB = rdyB ? tB : INF;
+            const uint64_t tmin = kF < kB ? kF : kB;
+            uint64_t key = tmin == INF ? INF : (tmin << 5) | (uint64_t)r;
+            uint64_t gk = group_min<G>(key);
+            bool relax = false;
+            if (__any_sync(FULL, gk == INF)) {             // stuck only because of gates? lift them (R-31)
+                const uint64_t k2 = rdyF ? ((tF << 5) | (uint64_t)r) : INF;
+                const uint64_t g2 = group_min<G>(k2);      // every lane shuffles; stuck groups use it
+                if (gk == INF) { gk = g2; relax = true; }
+            }
+            const uint32_t alive = __ballot_sync(FULL, !done);
+            if (alive == 0) break;
+            if (gk == INF && (alive & gmask)) {            // no rank of this group can place a stage: a cycle
+                dl = true;
+                done = true;
+            }
+            __syncwarp();
+            if (!done && gk != INF && (uint32_t)(gk & 31u) == (uint32_t)r) {
+                const bool fOK = rdyF && (!gated || relax);
+                const bool bOK = rdyB;
+                uint32_t dir;
+                if (fOK && bOK && tF < tlast && tB < tlast) dir = last == 0 ? 1u : 0u;   // emulate 1F1B
+                else if (!fOK) dir = 1u;
+                else if (!bOK) dir = 0u;
+                else dir = tB <= tF ? 1u : 0u;
+                const uint2 e = dir ? eB : eF;
+                const uint4 T = dir ? TB : TF;
+                const uint32_t lay = dir ? layB : layF;
+                const uint32_t idx = dir ? bi : fi;
+                const uint64_t ts = dir ? tB : tF;
+                const uint64_t st = ts > tlast ? ts : tlast;
+                const uint64_t end = st + (uint64_t)lay * (dir ? T.y : T.x);
+                busy += end - st;
+                tlast = end;
+                const uint32_t act = lay * T.z;
+                cur = dir ? cur - act : cur + act;
+                peak = cur > peak ? cur : peak;
+                const bool wrapP = dir ? isFirst : isLast;
+                uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)]
+                                     : &ringAll[(idx & (D - 1)) * P + (dir ? colOut1 : colOut0)];
+                const uint64_t pold = *pa;
+                const int32_t sgn = (int32_t)(e.x << 6) >> 30;
+                const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
+                const uint64_t cand2 = (pold & HIGH_MASK) | pv;
+                *pa = wrapP ? (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT) : end;
+                if (!wrapP) {
+                    const uint32_t ccnt = dir ? (up >> 16) : (dn & 0xFFFFu);   // consumer neighbour's count
+                    if (idx >= ccnt + D) spill_keep(spill, dir, r, P, n_max, idx, pold);
+                } else if (e.x & E_MULTI) {
+                    const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
+                    const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
+                    const uint32_t msk = dir ? mi[i].prod_mask : mi[i].cons_mask;
+                    for (uint32_t c = 0; c < nmod; c++) {
+                        if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                        uint64_t *sl = &depAll[dir ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
+                        const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
+                        *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                    }
+                }
+                const uint32_t t = fi + bi;
+                if (dir) wbuf |= 1u << (t & 31);
+                if ((t & 31) == 31 || t + 1 == S2) { fbOut[(t >> 5) * P] = wbuf; wbuf = 0; }
+                cnt += dir ? 0x10000u : 1u;
+                last = (int)dir;
+                done = t + 1 == S2;
+            }
+            __syncwarp();
+        }
+        if (dl && laneOn && wbuf) {                        // flush the partial word of a deadlocked build
+            const uint32_t t = (cnt & 0xFFFFu) + (cnt >> 16);
+            fbOut[(t >> 5) * P] = wbuf;
+        }
+        }
+
         // ---------------- results + K4 argmin ----------------
         const uint64_t mk = group_max<G>(tlast);
         const uint64_t bsum = group_sum<G>(busy);
@@ -494,7 +625,8 @@ __global__ void make_gkey(const unsigned long long *key, unsigned long long *gke
 
 template <int G>
 static cudaError_t launch_g(const KParams &kp, int grid, int block, size_t smem, cudaStream_t s) {
-    dip_eval_kernel<G><<<grid, block, smem, s>>>(kp);
+    if (kp.records_out) dip_eval_kernel<G, 1><<<grid, block, smem, s>>>(kp);
+    else dip_eval_kernel<G, 0><<<grid, block, smem, s>>>(kp);
     return cudaGetLastError();
 }
 
@@ -508,28 +640,44 @@ cudaError_t launch_eval(const KParams &kp, int G, int grid, int block, size_t sm
     }
 }
 
-template <int G>
-static const void *kfun() { return reinterpret_cast<const void *>(&dip_eval_kernel<G>); }
-static const void *kernel_for(int G) {
-    switch (G) {
-    case 4: return kfun<4>();
-    case 8: return kfun<8>();
-    case 16: return kfun<16>();
-    case 32: return kfun<32>();
+template <int G, int MODE>
+static const void *kfun() { return reinterpret_cast<const void *>(&dip_eval_kernel<G, MODE>); }
+static const void *kernel_for(int G, int mode) {
+    switch (G * 2 + mode) {
+    case 8: return kfun<4, 0>();
+    case 9: return kfun<4, 1>();
+    case 16: return kfun<8, 0>();
+    case 17: return kfun<8, 1>();
+    case 32: return kfun<16, 0>();
+    case 33: return kfun<16, 1>();
+    case 64: return kfun<32, 0>();
+    case 65: return kfun<32, 1>();
     default: return nullptr;
     }
 }
 
 cudaError_t prepare_eval(int G, size_t smem) {
-    const void *f = kernel_for(G);
-    if (!f) return cudaErrorInvalidValue;
-    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int mode = 0; mode < 2; mode++) {
+        const void *f = kernel_for(G, mode);
+        if (!f) return cudaErrorInvalidValue;
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm) {
-    const void *f = kernel_for(G);
-    if (!f) return cudaErrorInvalidValue;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+    int best = 1 << 30;
+    for (int mode = 0; mode < 2; mode++) {
+        const void *f = kernel_for(G, mode);
+        if (!f) return cudaErrorInvalidValue;
+        int b = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, block, smem);
+        if (e != cudaSuccess) return e;
+        best = b < best ? b : best;
+    }
+    *blocks_per_sm = best;
+    return cudaSuccess;
 }
 
 cudaError_t launch_scan_argmin(const dip_result *res, uint64_t count, uint64_t /*index_base*/,

@@ -84,6 +84,7 @@ def lib():
     L.dip_workspace_create.argtypes = [vp, ctypes.c_size_t, ctypes.POINTER(vp)]
     L.dip_workspace_free.argtypes = [vp]
     L.dip_eval_schedules.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
+    L.dip_interleave.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
     L.dip_argmin.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp,
                              ctypes.POINTER(_Winner), vp]
     L.dip_eval_host.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
@@ -95,7 +96,8 @@ def lib():
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
     for f in ("dip_load_cost_model", "dip_model_free", "dip_model_get_info", "dip_encode_candidates",
-              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_argmin", "dip_eval_host",
+              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_interleave", "dip_argmin",
+              "dip_eval_host",
               "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key"):
         getattr(L, f).restype = st
     L.dip_launch_count.restype = ctypes.c_uint64
@@ -249,6 +251,13 @@ class Comm:
 def eval_schedules(model: Model, ws: Workspace, d_records, count: int, d_results, d_peaks=None, stream=None):
     _check(lib().dip_eval_schedules(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results),
                                     _ptr(d_peaks), _stream(stream)), "dip_eval_schedules")
+
+
+def interleave(model: Model, ws: Workspace, d_records, count: int, d_results, d_peaks=None, stream=None):
+    """f1: build each record's F/B interleaving in place with DIP's dual-queue greedy
+    and score it (results as eval_schedules)."""
+    _check(lib().dip_interleave(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results),
+                                _ptr(d_peaks), _stream(stream)), "dip_interleave")
 
 
 def argmin(model: Model, ws: Workspace, count: int, shard_stride: Optional[int] = None, rank: int = 0,

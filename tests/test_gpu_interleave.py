@@ -1,0 +1,94 @@
+"""GPU (dip_interleave) vs the oracle's dual-queue greedy (I1-I6): the built
+F/B interleavings must be bit-identical, the scores equal, and re-scoring the built records with
+dip_eval_schedules must reproduce them (replay identity, App. A.8)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2504_14145_b200 as dip  # noqa: E402
+
+
+def fb_rows(pb, m, recs):
+    """Test-side reader of the records' word-major F/B rows -> [count, P, fbw]."""
+    n_pad = (pb.n_max + 7) // 8 * 8
+    nsplit = sum(1 for md in pb.modules if md.max_split > 1)
+    off_fwd = (4 + (pb.m * nsplit + 1) // 2 + 15) // 16 * 16
+    off_fb = (off_fwd + 4 * n_pad + 15) // 16 * 16
+    r = recs.reshape(-1, m.stride)[:, off_fb:off_fb + 4 * pb.fbw * pb.P]
+    return np.ascontiguousarray(r).view(np.uint32).reshape(-1, pb.fbw, pb.P).transpose(0, 2, 1)
+
+
+def run_interleave(pb, cs):
+    m = dip.Model(pb, 0)
+    ws = dip.Workspace(m)
+    s = torch.cuda.current_stream()
+    d_rec = torch.from_numpy(m.encode(cs)).cuda()
+    d_res = torch.empty(cs.count * 24, dtype=torch.uint8, device="cuda")
+    d_pk = torch.empty((cs.count, pb.P), dtype=torch.int32, device="cuda")
+    dip.interleave(m, ws, d_rec, cs.count, d_res, d_pk, stream=s)
+    win = dip.argmin(m, ws, cs.count, stream=s)
+    res = dip.results_view(d_res.cpu().numpy()).copy()
+    pk = d_pk.cpu().numpy().view(np.uint32).copy()
+    bits = fb_rows(pb, m, d_rec.cpu().numpy())
+    # replay: score the built records with the fixed-order scorer
+    d_res2 = torch.empty_like(d_res)
+    dip.eval_schedules(m, ws, d_rec, cs.count, d_res2, d_pk, stream=s)
+    res2 = dip.results_view(d_res2.cpu().numpy())
+    torch.cuda.synchronize()
+    return res, pk, bits, win, res2, d_pk.cpu().numpy().view(np.uint32)
+
+
+def check(pb, cs):
+    res, pk, bits, win, res2, pk2 = run_interleave(pb, cs)
+    rbits, ref = oracle.interleave(pb, cs, threads=16)
+    assert np.array_equal(res["status"], ref.status), np.nonzero(res["status"] != ref.status)[0][:8]
+    assert np.array_equal(bits, rbits), np.nonzero((bits != rbits).any(axis=(1, 2)))[0][:8]
+    assert np.array_equal(res["makespan_ns"], ref.makespan)
+    assert np.array_equal(res["oom_mask"], ref.oom_mask)
+    assert np.array_equal(res["bubble"].view(np.uint64), ref.bubble.view(np.uint64))
+    assert np.array_equal(pk.astype(np.uint64), ref.peaks)
+    best = oracle.argmin(ref.makespan, ref.status)
+    assert win.found == (best >= 0) and (best < 0 or win.global_index == best)
+    timed = (ref.status == oracle.ST_OK) | (ref.status == oracle.ST_OOM)
+    assert np.array_equal(res2["makespan_ns"][timed], res["makespan_ns"][timed])     # replay identity
+    assert np.array_equal(res2["status"][timed], res["status"][timed])
+    assert np.array_equal(pk2[timed], pk[timed])
+    return res
+
+
+@pytest.mark.parametrize("name,count", [("toy", 256), ("12B", 512), ("37B", 256), ("T2V", 128), ("94B", 48)])
+def test_interleave_parity(name, count):
+    pb = gen.make_problem(name)
+    cs = gen.generate(pb, 0, count, mode=1 if name == "toy" else 0, p_mutate=0.0, p_bad=0.02)
+    check(pb, cs)
+
+
+def test_interleave_paper_pins_on_gpu():
+    # App. A.8: gated with (P - r) activations -> exact 1F1B orders; ungated -> the 1F1B makespan
+    for P, m_ in [(4, 8), (8, 16), (3, 5)]:
+        pb = H.uniform_problem(P, m_, 1, 2, act=2, budget=[(P - r) * 2 for r in range(P)])
+        cs = H.candidates_from_orders(pb, [[1] * m_], [H.one_f_one_b(P, m_)])
+        res, pk, bits, win, _, _ = run_interleave(pb, cs)
+        assert np.array_equal(bits[0], cs.fb[0]) and int(res["makespan_ns"][0]) == (m_ + P - 1) * 3
+    pb = H.uniform_problem(8, 16, 1, 2, act=1)
+    cs = H.candidates_from_orders(pb, [[1] * 16], [H.one_f_one_b(8, 16)])
+    res, pk, bits, win, _, _ = run_interleave(pb, cs)
+    assert pk[0].tolist() == [16, 16, 16, 15, 14, 10, 6, 2]
+
+
+def test_interleave_deadlock_and_bad():
+    pb = H.uniform_problem(2, 1, 1, 2, K=2)
+    cs = H.candidates_from_orders(pb, [[1]], [[[("F", 0), ("F", 1), ("B", 1), ("B", 0)]] * 2])
+    c = cs.subset([0, 0])
+    c.fwd[0, :2] = [1, 0]          # not a linear extension -> DEADLOCK
+    c.fwd[1, 1] = c.fwd[1, 0]      # duplicate id -> BAD_ENCODING
+    res = check(pb, c)
+    assert res["status"].tolist() == [oracle.ST_DEADLOCK, oracle.ST_BAD]
