@@ -171,6 +171,9 @@ def main():
     ap.add_argument("--host-chunk", type=int, default=65536)
     ap.add_argument("--f1-count", type=int, default=65536,
                     help="candidates for the f1 (dual-queue interleaving) measurement; 0 disables it")
+    ap.add_argument("--f2-rounds", type=int, default=8, help="MCTS rounds for the f2 measurement; 0 disables it")
+    ap.add_argument("--f2-leaves", type=int, default=256)
+    ap.add_argument("--f2-rollouts", type=int, default=10)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -305,6 +308,21 @@ def main():
                                 "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
         del d_f1, r_f1
 
+    # ---- MCTS segment reordering with batched GPU rollouts, for the
+    # split of candidate 0 of this shard (rank 0 only; a search is one planner's job)
+    f2 = None
+    if args.f2_rounds > 0 and rank == 0:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sr = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,
+                        rollouts=args.f2_rollouts, alpha=1.0, beta=0.5, stream=stream)
+        dt = time.perf_counter() - t0
+        f2 = {"what": "dip_search: MCTS over class priorities (P:472-509), rollouts = priorities -> f1 interleaving "
+                      "-> score, one batched GPU launch per round",
+              "rollouts_per_s": sr["scored"] / dt, "rollouts": sr["scored"], "rounds": sr["rounds_done"],
+              "wall_s": dt, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
+              "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"]}
+
     hbm_peak, sm_max, src = peaks()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -336,7 +354,7 @@ def main():
             "hbm": {"achieved": bytes_launch / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bytes_launch / kern_s / 1e9 / hbm_peak,
                     "algorithmic": "record + 24 B result + 4P B peaks per candidate", "peak_source": src},
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks, "f1_interleave": f1,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks, "f1_interleave": f1, "f2_search": f2,
             "status_hist": {"ok": hist[0], "oom": hist[1], "deadlock": hist[2], "bad_encoding": hist[3]},
             "winner": {"found": win.found, "global_index": win.global_index, "makespan_ns": win.makespan_ns},
             "setup_s": {"generate": round(t_gen, 1)},

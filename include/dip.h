@@ -149,6 +149,12 @@ dip_status dip_workspace_free(dip_workspace *w);
 dip_status dip_eval_schedules(const dip_model *m, dip_workspace *w, const void *d_records, size_t count,
                               dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
 
+/* dip_eval_schedules plus every stage's simulated start / end time: d_start / d_end are device
+ * [count][P][2*n_max] u64, entry (c, r, t) = rank r's slot t of candidate c (zero beyond 2n and for
+ * candidates that are not timed). For Gantt charts and the plan compiler (f4). Asynchronous. */
+dip_status dip_timeline(const dip_model *m, dip_workspace *w, const void *d_records, size_t count,
+                        dip_result *d_results, uint64_t *d_start, uint64_t *d_end, void *stream);
+
 /* DIP's greedy dual-queue stage interleaving (§5.2):
  * for every record, take its split and its forward / backward segment orders as the priority
  * orders of the per-rank queues, build each rank's F/B interleaving with the paper's iterative
@@ -160,6 +166,40 @@ dip_status dip_eval_schedules(const dip_model *m, dip_workspace *w, const void *
  * updated as by dip_eval_schedules (dip_argmin works after it). Asynchronous on `stream`. */
 dip_status dip_interleave(const dip_model *m, dip_workspace *w, void *d_records, size_t count,
                           dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+
+/* DIP's MCTS segment reordering (§5.1) with batched
+ * GPU rollouts. For the given split, classes = (direction, microbatch, module) with M > 0 (one
+ * priority per modality per microbatch, fixed internal order); a sequence of classes
+ * gives priorities (position p -> Cn-1-p) -> forward / backward priority orders -> f1
+ * interleaving -> score LB / makespan (0 if not OK; LB = busiest rank's total latency). Each
+ * round selects `leaves` leaves by UCB s^alpha + beta*sqrt(ln N_parent / N_child) with
+ * virtual visits, expands one child each (next class in order), scores `rollouts` random
+ * completions per leaf in one dip_interleave launch and backpropagates the best trial
+ * (s = max, N + 1). Deterministic for a seed (rollout u draws from splitmix64(seed, u)).
+ * Allocates its rollout buffers for the duration of the call. Synchronous. */
+typedef struct {
+    uint64_t seed;
+    uint32_t rounds;          /* search rounds */
+    uint32_t leaves;          /* leaves expanded per round (one batched GPU launch) */
+    uint32_t rollouts;        /* random completions per leaf ("e.g., 10 trials") */
+    int32_t threads;          /* host threads building rollout records (<= 0: all cores) */
+    double alpha, beta;       /* UCB hyper-parameters */
+} dip_search_params;
+
+typedef struct {
+    int32_t found;            /* a feasible (status OK) schedule was found */
+    uint32_t rounds_done;
+    uint64_t makespan_ns;     /* of the best schedule */
+    double score;             /* LB / makespan of the best schedule */
+    uint64_t rollouts_scored;
+    uint64_t tree_nodes;
+} dip_search_result;
+
+/* best_record_out: host buffer of record_stride bytes receiving the best schedule (split, priority
+ * orders and its interleaved F/B bits), or NULL; trace: [rounds] best score after each round, or NULL. */
+dip_status dip_search(const dip_model *m, dip_workspace *w, const uint8_t *split /* [m*n_modules] */,
+                      const dip_search_params *p, void *best_record_out, double *trace,
+                      dip_search_result *out, void *stream);
 
 typedef struct {
     int32_t found;            /* 0 if no candidate has status OK on any rank */
@@ -190,6 +230,33 @@ dip_status dip_unpack_key(uint64_t key, uint64_t shard_stride, uint32_t world, d
 dip_status dip_eval_host(const dip_model *m, dip_workspace *w, const void *h_records, size_t count,
                          dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world,
                          dip_comm *comm, dip_winner *out, void *stream);
+
+/* compile one scored schedule into per-rank action lists (§6.3,
+ * P:717-734): fw_stage / bw_stage per stage; for every cross-rank dependency edge an asynchronous
+ * isend right after the producing stage, wait_isend before the producer's next stage, irecv right
+ * after the consumer's last stage that ends no later than the producer starts (so every receive is
+ * posted before its send in simulated time) and wait_irecv right before the consuming stage;
+ * consecutive isend / irecv actions share a batch id ("grouped into a batched operation").
+ * record: one host record (as encoded / interleaved); start / end: its host timeline rows
+ * ([P][2*n_max], from dip_timeline). actions: capacity entries, rank r's list is
+ * actions[rank_off[r] .. rank_off[r+1]). DIP_ERANGE if capacity is too small (rank_off[P] = size). */
+enum { DIP_ACT_FW_STAGE = 0, DIP_ACT_BW_STAGE = 1, DIP_ACT_ISEND = 2, DIP_ACT_IRECV = 3,
+       DIP_ACT_WAIT_ISEND = 4, DIP_ACT_WAIT_IRECV = 5 };
+typedef struct {
+    uint32_t kind;            /* DIP_ACT_* */
+    uint32_t peer;            /* P2P: the other rank; stages: own rank */
+    uint32_t tag;             /* P2P: message tag (dense, in compile order); stages: segment id */
+    uint32_t batch;           /* P2P: batch id (consecutive P2P actions share one); stages: 0 */
+    uint32_t slot;            /* the stage slot the action belongs to */
+} dip_action;
+dip_status dip_compile_plan(const dip_model *m, const void *record, const uint64_t *start, const uint64_t *end,
+                            dip_action *actions, size_t capacity, uint32_t *rank_off /* [P+1] */,
+                            uint32_t *n_messages);
+/* Discrete-event execution of a plan (P2P priced as on the schedule's edges): *ok = 1 iff every
+ * isend / irecv tag is perfectly paired and the plan terminates; stage_start ([P][2*n_max], or
+ * NULL) receives each stage's start time, which equals the source timeline for compiled plans. */
+dip_status dip_validate_plan(const dip_model *m, const void *record, const dip_action *actions,
+                             const uint32_t *rank_off, uint64_t *stage_start, int32_t *ok);
 
 /* NCCL communicator for the argmin: rank 0 calls dip_comm_unique_id, broadcasts
  * the 128 bytes (e.g. over torch.distributed), every rank calls dip_comm_init. */

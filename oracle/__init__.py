@@ -30,7 +30,7 @@ ST_OK, ST_OOM, ST_DEADLOCK, ST_BAD = 0, 1, 2, 3
 def build(force: bool = False) -> str:
     """Compile the oracle with plain -O2 (no SIMD tricks: it is the slow reference)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", _SO, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", _SO, _SRC, "-lm"])
     return _SO
 
 
@@ -64,6 +64,10 @@ def _load():
         lib.oracle_interleave.restype = ctypes.c_int
         lib.oracle_interleave.argtypes = [ctypes.POINTER(_OProblem), ctypes.POINTER(_OCands), ctypes.c_uint64,
                                           ctypes.c_uint64] + [ctypes.c_void_p] * 7 + [ctypes.c_int]
+        lib.oracle_search.restype = ctypes.c_int
+        lib.oracle_search.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                                      ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_double, ctypes.c_double] + [ctypes.c_void_p] * 7
         lib.oracle_argmin.restype = ctypes.c_int64
         lib.oracle_argmin.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
         _lib = lib
@@ -145,6 +149,27 @@ def interleave(pb, cands, first: int = 0, count: Optional[int] = None, threads: 
                                res.bubble.ctypes.data, res.peaks.ctypes.data, res.busy.ctypes.data, threads)
     assert rc == 0
     return bits, res
+
+
+def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float = 1.0, beta: float = 0.5):
+    """S1-S6: MCTS over class orders with batched rounds, scoring rollouts with I1-I6.
+    Returns dict(score, makespan, trace, fwd, bwd, bits, scored)."""
+    from gen import Candidates
+    lib = _load()
+    dummy = Candidates(pb, 1)
+    bd = _Bound(pb, dummy)
+    sp = np.ascontiguousarray(np.asarray(split, np.uint8).reshape(-1))
+    trace = np.zeros(rounds, np.float64)
+    sc = ctypes.c_double()
+    mk = ctypes.c_uint64()
+    scored = ctypes.c_uint64()
+    fwd = np.zeros(pb.n_max, np.uint16)
+    bwd = np.zeros(pb.n_max, np.uint16)
+    bits = np.zeros((pb.P, pb.fbw), np.uint32)
+    lib.oracle_search(ctypes.byref(bd.pb), pb.n_max, pb.fbw, sp.ctypes.data, seed & ((1 << 64) - 1), rounds, leaves,
+                      rollouts, alpha, beta, trace.ctypes.data, ctypes.byref(sc), ctypes.byref(mk), fwd.ctypes.data,
+                      bwd.ctypes.data, bits.ctypes.data, ctypes.byref(scored))
+    return dict(score=sc.value, makespan=mk.value, trace=trace, fwd=fwd, bwd=bwd, bits=bits, scored=scored.value)
 
 
 def timeline(pb, cands, x: int):

@@ -20,11 +20,13 @@
  *   O10 outputs            P:499 score = "end-to-end iteration time"; bubble P:248 (R-16)
  *   O11 argmin             P:499-501 best score; ties -> lowest index (R-14, R-15)
  *   I1-I6 interleaving     P:511-548 the dual-queue greedy, see below
+ *   S1-S6 search           P:472-509 MCTS segment reordering, see below
  *
  * Integers everywhere (ns, KiB); u64 accumulators.  The only floating-point
  * value, the bubble ratio, is one IEEE double division of two exact integers.
  * Multi-threaded only across candidates (pthreads).
  */
+#include <math.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -612,6 +614,243 @@ int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint
         pthread_create(&th[t], NULL, iworker, &jobs[t]);
     }
     for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+    return 0;
+}
+
+/* ======================================================================================
+ * S1-S6: DIP's MCTS segment reordering (§5.1), the row f2 of SURVEY §8(f),
+ * written step by step from the paper with the readings of DESIGN.md §3 (R-32..R-35):
+ *   S1 classes: (direction, microbatch b, module i) with M_{b,i} > 0 -- same-modality segments of
+ *      one microbatch share a priority and keep a fixed order; forward classes in
+ *      (b, i) order, then the backward classes in the same order.
+ *   S2 a sequence (permutation of the Cn classes) gives priority Cn-1-p to the class at position p
+ *      (P:481); the forward / backward queue order of a rank = repeatedly the ready segment of the
+ *      highest priority (within a class: j ascending, k ascending for F / descending for B).
+ *   S3 rollout score: interleave (I1-I6) and score LB / makespan if OK, else 0, with LB the
+ *      busiest rank's summed latency of the split.
+ *   S4 selection: from the root, while the node has all its children, move to the child of
+ *      largest s^alpha + beta * sqrt(ln N_x / N_v) (ties: first child, i.e. lowest class); counts
+ *      include the virtual visits of the current round.
+ *   S5 expansion: add the child of the next unused class in class order; rollouts:
+ *      `rollouts` uniformly random completions (one if the sequence is complete), the u-th rollout
+ *      drawing from a splitmix64 stream seeded with splitmix64(seed ^ splitmix64(u + 0x51A9)).
+ *   S6 backpropagation: along the path, s = max(s, best trial), N += 1.
+ *   A round selects `leaves` leaves (virtual visit on every node of each path), then scores all
+ *   their rollouts, then backpropagates leaf by leaf.
+ * ====================================================================================== */
+static uint64_t smix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+typedef struct { int parent, cls, depth, nch, cap; int *ch; double s; uint32_t N, vl; } snode;
+
+/* S2: queue order of one direction from class priorities (plain selection, O(n^2)) */
+static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *base, const int *clsof, uint32_t C,
+                    uint32_t Cn, const uint32_t *prio, int dir, uint32_t n_max, uint16_t *out) {
+    const uint32_t nm = pb->nmod, m = pb->m;
+    uint32_t idmax = seg_count_max(pb);
+    int32_t *indeg = malloc(sizeof(int32_t) * (idmax + 1));
+    uint64_t *key = malloc(sizeof(uint64_t) * (idmax + 1));
+    uint8_t *ready = calloc(idmax + 1, 1);
+    uint32_t n = 0;
+    for (uint32_t x = 0; x <= idmax; x++) indeg[x] = -1;
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            uint32_t q = b * nm + i, K = pb->K[i];
+            for (uint32_t j = 0; j < split[q]; j++)
+                for (uint32_t k = 0; k < K; k++) {
+                    uint32_t s = base[q] + j * K + k;
+                    int32_t d = 0;
+                    if (dir == 0) {
+                        if (k > 0) d = 1;
+                        else for (uint32_t p = 0; p < nm; p++) if ((pb->producer_mask[i] >> p) & 1u) d += split[b * nm + p];
+                    } else {
+                        if (k + 1 < K) d = 1;
+                        else for (uint32_t c = 0; c < nm; c++) if ((pb->producer_mask[c] >> i) & 1u) d += split[b * nm + c];
+                    }
+                    indeg[s] = d;
+                    uint32_t c = (uint32_t)clsof[q] + (dir ? C : 0);
+                    key[s] = ((uint64_t)(Cn - 1 - prio[c]) << 40) | ((uint64_t)j << 24) | ((uint64_t)(dir ? K - 1 - k : k) << 12);
+                    if (d == 0) ready[s] = 1;
+                    n++;
+                }
+        }
+    for (uint32_t cnt = 0; cnt < n; cnt++) {
+        uint32_t pick = 0xFFFFFFFFu;
+        for (uint32_t s = 0; s < idmax; s++)
+            if (ready[s] && (pick == 0xFFFFFFFFu || key[s] < key[pick])) pick = s;
+        out[cnt] = (uint16_t)pick;
+        ready[pick] = 0;
+        /* successors of pick in this direction */
+        uint32_t q = 0;
+        while (q + 1 < m * nm && base[q + 1] <= pick) q++;
+        uint32_t b = q / nm, i = q % nm, K = pb->K[i], k = (pick - base[q]) % K;
+        if (dir == 0) {
+            if (k + 1 < K) { if (--indeg[pick + 1] == 0) ready[pick + 1] = 1; }
+            else for (uint32_t c = 0; c < nm; c++)
+                if ((pb->producer_mask[c] >> i) & 1u)
+                    for (uint32_t jj = 0; jj < split[b * nm + c]; jj++) {
+                        uint32_t t = base[b * nm + c] + jj * pb->K[c];
+                        if (--indeg[t] == 0) ready[t] = 1;
+                    }
+        } else {
+            if (k > 0) { if (--indeg[pick - 1] == 0) ready[pick - 1] = 1; }
+            else for (uint32_t p = 0; p < nm; p++)
+                if ((pb->producer_mask[i] >> p) & 1u)
+                    for (uint32_t jj = 0; jj < split[b * nm + p]; jj++) {
+                        uint32_t t = base[b * nm + p] + jj * pb->K[p] + pb->K[p] - 1;
+                        if (--indeg[t] == 0) ready[t] = 1;
+                    }
+        }
+    }
+    for (uint32_t p = n; p < n_max; p++) out[p] = 0xFFFF;
+    free(indeg); free(key); free(ready);
+}
+
+int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_t *split, uint64_t seed,
+                  uint32_t rounds, uint32_t leaves, uint32_t rollouts, double alpha, double beta,
+                  double *trace, double *best_score, uint64_t *best_makespan, uint16_t *best_fwd,
+                  uint16_t *best_bwd, uint32_t *best_bits, uint64_t *scored_out) {
+    const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
+    uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
+    int *clsof = malloc(sizeof(int) * m * nm);
+    uint32_t acc = 0, C = 0, n = 0;
+    for (uint32_t q = 0; q < m * nm; q++) {
+        base[q] = acc;
+        acc += pb->max_split[q % nm] * pb->K[q % nm];
+        clsof[q] = split[q] ? (int)C++ : -1;
+        n += split[q] * pb->K[q % nm];
+    }
+    const uint32_t Cn = 2 * C;
+    *best_score = 0.0;
+    *best_makespan = UINT64_MAX;
+    *scored_out = 0;
+    if (C == 0) { free(base); free(clsof); return 0; }
+    /* S3: LB = the busiest rank's summed latency of this split (O1, O2 of the fixed-order oracle) */
+    double LB = 0.0;
+    for (uint32_t r = 0; r < P; r++) {
+        uint64_t tot = 0;
+        for (uint32_t q = 0; q < m * nm; q++) {
+            uint32_t i = q % nm, Mv = split[q];
+            if (!Mv) continue;
+            uint32_t lo = pb->inst_off[q], N = pb->inst_off[q + 1] - lo, st[16];
+            oracle_split(N, Mv, st);
+            for (uint32_t j = 0; j < Mv; j++) {
+                uint32_t w = 0;
+                for (uint32_t x = st[j]; x < st[j + 1]; x++) w += pb->inst_units[lo + x];
+                for (uint32_t k = 0; k < pb->K[i]; k++)
+                    tot += (uint64_t)layers_of(pb, i, k * P + r) *
+                           ((uint64_t)pb->tab_f[pb->tab_off[i] + w] + pb->tab_b[pb->tab_off[i] + w]);
+            }
+        }
+        if ((double)tot > LB) LB = (double)tot;
+    }
+    uint32_t ncap = 1 + rounds * leaves, nn = 1;
+    snode *T = calloc(ncap, sizeof(snode));
+    T[0].parent = -1; T[0].cls = -1; T[0].depth = 0;
+    uint32_t maxr = leaves * rollouts;
+    uint8_t *spl = malloc((size_t)maxr * m * nm);
+    uint32_t *nn_ = malloc(sizeof(uint32_t) * maxr);
+    uint16_t *fw = malloc(sizeof(uint16_t) * (size_t)maxr * n_max), *bw = malloc(sizeof(uint16_t) * (size_t)maxr * n_max);
+    uint32_t *fb = calloc((size_t)maxr * P * fbw, sizeof(uint32_t)), *bits = malloc(sizeof(uint32_t) * (size_t)maxr * P * fbw);
+    int *owner = malloc(sizeof(int) * maxr), *leaf = malloc(sizeof(int) * leaves);
+    uint32_t *seq = malloc(sizeof(uint32_t) * Cn), *prio = malloc(sizeof(uint32_t) * Cn), *rest = malloc(sizeof(uint32_t) * Cn);
+    uint8_t *used = malloc(Cn);
+    double best = -1.0;
+    uint64_t u = 0;
+    for (uint32_t rd = 0; rd < rounds; rd++) {
+        uint32_t cnt = 0;
+        for (uint32_t l = 0; l < leaves; l++) {
+            int v = 0;
+            memset(used, 0, Cn);
+            for (;;) {                                           /* S4 / S5 */
+                snode *nd = &T[v];
+                if ((uint32_t)nd->depth == Cn) break;
+                if ((uint32_t)nd->nch < Cn - nd->depth) {
+                    uint32_t c, seen = 0;
+                    for (c = 0; c < Cn; c++) { if (used[c]) continue; if (seen++ == (uint32_t)nd->nch) break; }
+                    int id = (int)nn++;
+                    T[id].parent = v; T[id].cls = (int)c; T[id].depth = nd->depth + 1;
+                    if (nd->nch == nd->cap) { nd->cap = nd->cap ? 2 * nd->cap : 4; nd->ch = realloc(nd->ch, sizeof(int) * nd->cap); }
+                    nd->ch[nd->nch++] = id;
+                    used[c] = 1;
+                    v = id;
+                    break;
+                }
+                double Nx = (double)(nd->N + nd->vl), bu = -1.0;
+                int bc = -1;
+                for (int x = 0; x < nd->nch; x++) {
+                    snode *cn = &T[nd->ch[x]];
+                    double Nv = (double)(cn->N + cn->vl);
+                    double ucb = pow(cn->s, alpha) + beta * sqrt(log(Nx) / Nv);
+                    if (ucb > bu) { bu = ucb; bc = nd->ch[x]; }
+                }
+                used[T[bc].cls] = 1;
+                v = bc;
+            }
+            for (int x = v; x >= 0; x = T[x].parent) T[x].vl++;
+            leaf[l] = v;
+            uint32_t d = (uint32_t)T[v].depth;
+            for (int x = v; x > 0; x = T[x].parent) seq[T[x].depth - 1] = (uint32_t)T[x].cls;
+            uint32_t trials = d == Cn ? 1 : rollouts;
+            for (uint32_t tr = 0; tr < trials; tr++) {
+                uint32_t nr = 0;
+                for (uint32_t c = 0; c < Cn; c++) {
+                    int on = 0;
+                    for (uint32_t p = 0; p < d; p++) if (seq[p] == c) on = 1;
+                    if (!on) rest[nr++] = c;
+                }
+                uint64_t rs = smix(seed ^ smix(u + 0x51A9u));
+                for (uint32_t x = nr; x > 1; x--) {
+                    rs += 0x9E3779B97F4A7C15ull;
+                    uint32_t y = (uint32_t)(smix(rs) % x), t2 = rest[x - 1];
+                    rest[x - 1] = rest[y]; rest[y] = t2;
+                }
+                for (uint32_t x = 0; x < nr; x++) seq[d + x] = rest[x];
+                for (uint32_t p = 0; p < Cn; p++) prio[seq[p]] = Cn - 1 - p;
+                memcpy(spl + (size_t)cnt * m * nm, split, m * nm);
+                nn_[cnt] = n;
+                s_order(pb, split, base, clsof, C, Cn, prio, 0, n_max, fw + (size_t)cnt * n_max);
+                s_order(pb, split, base, clsof, C, Cn, prio, 1, n_max, bw + (size_t)cnt * n_max);
+                owner[cnt] = (int)l;
+                cnt++;
+                u++;
+            }
+        }
+        /* S3: score every rollout of the round */
+        ocands cs = {n_max, fbw, spl, nn_, fw, bw, fb};
+        double *lb = calloc(leaves, sizeof(double));
+        for (uint32_t x = 0; x < cnt; x++) {
+            ores r;
+            interleave_one(pb, &cs, x, bits + (size_t)x * P * fbw, &r, NULL);
+            double sc = r.status == ST_OK ? LB / (double)r.makespan : 0.0;
+            if (sc > lb[owner[x]]) lb[owner[x]] = sc;
+            if (sc > best) {
+                best = sc;
+                *best_makespan = r.makespan;
+                if (best_fwd) memcpy(best_fwd, fw + (size_t)x * n_max, sizeof(uint16_t) * n_max);
+                if (best_bwd) memcpy(best_bwd, bw + (size_t)x * n_max, sizeof(uint16_t) * n_max);
+                if (best_bits) memcpy(best_bits, bits + (size_t)x * P * fbw, sizeof(uint32_t) * P * fbw);
+            }
+        }
+        *scored_out += cnt;
+        for (uint32_t l = 0; l < leaves; l++)                       /* S6 */
+            for (int x = leaf[l]; x >= 0; x = T[x].parent) {
+                if (lb[l] > T[x].s) T[x].s = lb[l];
+                T[x].N++;
+                T[x].vl--;
+            }
+        free(lb);
+        if (trace) trace[rd] = best;
+    }
+    *best_score = best > 0.0 ? best : 0.0;
+    for (uint32_t x = 0; x < nn; x++) free(T[x].ch);
+    free(T); free(spl); free(nn_); free(fw); free(bw); free(fb); free(bits); free(owner); free(leaf);
+    free(seq); free(prio); free(rest); free(used); free(base); free(clsof);
     return 0;
 }
 

@@ -20,76 +20,16 @@
 #include <vector>
 
 #include "dip.h"
+#include "dip_host_internal.h"
 #include "dip_internal.h"
 
 using dipk::KParams;
 using dipk::ModInfo;
 
-namespace {
+thread_local std::string diph::g_err;
+std::atomic<uint64_t> diph::g_launches{0};
 
-thread_local std::string g_err;
-std::atomic<uint64_t> g_launches{0};
-
-dip_status fail(dip_status s, const std::string &msg) {
-    g_err = msg;
-    return s;
-}
-#define CUDA_TRY(x)                                                                            \
-    do {                                                                                       \
-        cudaError_t _e = (x);                                                                  \
-        if (_e != cudaSuccess) return fail(DIP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
-    } while (0)
-#define NCCL_TRY(x)                                                                            \
-    do {                                                                                       \
-        ncclResult_t _r = (x);                                                                 \
-        if (_r != ncclSuccess) return fail(DIP_ENCCL, std::string(#x) + ": " + ncclGetErrorString(_r)); \
-    } while (0)
-
-inline uint32_t up16(uint32_t x) { return (x + 15u) & ~15u; }
-inline uint32_t bits_for(uint64_t n) {   // smallest b >= 1 with n <= 2^b
-    uint32_t b = 1;
-    while (b < 63 && (1ull << b) < n) b++;
-    return b;
-}
-
-}  // namespace
-
-struct dip_model {
-    int device = 0;
-    uint32_t P = 0, nmod = 0, m = 0, n_max = 0, n_pad = 0, fbw = 0, stride = 0;
-    uint32_t off_nib = 0, off_fwd = 0, off_bwd = 0, off_fb = 0, nsplit = 0;
-    std::vector<uint32_t> max_split, nib_slot, nbi;   // host copies for encode
-    std::vector<uint8_t> blob;
-    uint8_t *d_blob = nullptr;
-    KParams kp{};                  // shape + blob + layout; per-launch fields filled per call
-    int G = 32, cpg = 1, wpb = 1, bps = 1, grid = 1, num_sms = 148;
-    size_t smem = 0;
-    uint64_t mk_bound = 0;
-};
-
-struct dip_workspace {
-    const dip_model *model = nullptr;
-    unsigned long long *d_misc = nullptr;   // [0] counter [1] key [2] gkey [3] mk [4] idx [5..] spare
-    unsigned long long *h_misc = nullptr;   // pinned
-    unsigned long long *d_spill = nullptr;
-    size_t spill_bytes = 0;
-    // last eval
-    const dip_result *last_results = nullptr;
-    uint64_t last_count = 0;
-    uint32_t last_idx_bits = 1;
-    bool last_fused = true;
-    // host path
-    size_t host_chunk = 0;
-    uint8_t *d_rec[2] = {nullptr, nullptr};
-    dip_result *d_res = nullptr;           // [count capacity] grows on demand? fixed: 2 * host_chunk
-    cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-};
-
-struct dip_comm {
-    ncclComm_t comm = nullptr;
-    int rank = 0, world = 1;
-};
+using namespace diph;
 
 static void fill_shape(dip_model *M) {
     KParams &kp = M->kp;
@@ -270,6 +210,20 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     kp.nslotB = nslotB;
     blob.resize(up16((uint32_t)blob.size()));
     kp.blob_bytes = (uint32_t)blob.size();
+
+    // host copies of the structure and tables (used by the search, f2)
+    for (uint32_t i = 0; i < nm; i++) {
+        M->Kv.push_back(mi[i].K);
+        M->prod_mask.push_back(mi[i].prod_mask);
+        M->cons_mask.push_back(mi[i].cons_mask);
+        M->tab_off.push_back(mi[i].tab_off);
+        M->lay_off.push_back(mi[i].lay_off);
+    }
+    M->tab = tab;
+    M->layers = layers;
+    M->woff = woff;
+    M->wtab = wtab;
+    M->sbase = sbase;
 
     // ---- record layout
     M->n_max = n_max;
@@ -452,12 +406,15 @@ dip_status dip_workspace_free(dip_workspace *w) {
 }
 
 // ---------------------------------------------------------------- eval -----------------
-static dip_status launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
+extern "C++" {
+dip_status diph::launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                                uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
-                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out = nullptr) {
+                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out) {
     KParams kp = M->kp;
     kp.records = static_cast<const uint8_t *>(d_records);
     kp.records_out = records_out;
+    kp.tl_start = nullptr;
+    kp.tl_end = nullptr;
     kp.count = count;
     kp.index_base = index_base;
     kp.results = d_results;
@@ -475,9 +432,10 @@ static dip_status launch_chunk(const dip_model *M, dip_workspace *w, const void 
     return DIP_OK;
 }
 
-static bool fused_ok(const dip_model *M, uint32_t idx_bits) {
+bool diph::fused_ok(const dip_model *M, uint32_t idx_bits) {
     return idx_bits < 63 && (M->mk_bound >> (64 - idx_bits)) == 0;
 }
+}  // extern "C++"
 
 dip_status dip_eval_schedules(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                               dip_result *d_results, uint32_t *d_peaks, void *stream) {
@@ -510,6 +468,41 @@ dip_status dip_interleave(const dip_model *M, dip_workspace *w, void *d_records,
     if (!count) return DIP_OK;
     return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s,
                         static_cast<uint8_t *>(d_records));
+}
+
+dip_status dip_timeline(const dip_model *M, dip_workspace *w, const void *d_records, size_t count, dip_result *d_results,
+                        uint64_t *d_start, uint64_t *d_end, void *stream) {
+    if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
+    if (count && (!d_records || !d_results || !d_start || !d_end)) return fail(DIP_EINVAL, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
+    w->last_results = d_results;
+    w->last_count = count;
+    w->last_idx_bits = bits_for(std::max<uint64_t>(count, 2));
+    w->last_fused = fused_ok(M, w->last_idx_bits);
+    if (!count) return DIP_OK;
+    KParams kp = M->kp;
+    kp.records = static_cast<const uint8_t *>(d_records);
+    kp.records_out = nullptr;
+    kp.tl_start = d_start;
+    kp.tl_end = d_end;
+    kp.count = count;
+    kp.index_base = 0;
+    kp.results = d_results;
+    kp.peaks = nullptr;
+    kp.counter = w->d_misc + 0;
+    kp.best_key = w->d_misc + 1;
+    kp.spill = w->d_spill;
+    kp.fused_key = w->last_fused ? 1u : 0u;
+    kp.idx_bits = w->last_idx_bits;
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 0, 0, sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(d_start, 0, count * M->P * 2ull * M->n_max * 8, s));
+    CUDA_TRY(cudaMemsetAsync(d_end, 0, count * M->P * 2ull * M->n_max * 8, s));
+    const int grid = (int)std::min<uint64_t>((uint64_t)M->grid,
+                                             std::max<uint64_t>(1, (count + M->cpg * M->wpb - 1) / (M->cpg * M->wpb)));
+    CUDA_TRY(dipk::launch_eval(kp, M->G, grid, M->wpb * 32, M->smem, s));
+    g_launches++;
+    return DIP_OK;
 }
 
 // local winner -> (makespan, local index) on the host; exact two-pass scan when not fused

@@ -38,6 +38,7 @@ struct KParams {
     // per launch
     const uint8_t *records;
     uint8_t *records_out;       // non-null: interleave mode (f1) writes the F/B bit rows here
+    uint64_t *tl_start, *tl_end;  // non-null: timeline mode, [count][P][2*n_max] per-slot start / end
     uint64_t count, index_base;
     dip_result *results;
     uint32_t *peaks;

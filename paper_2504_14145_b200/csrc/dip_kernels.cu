@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             uint32_t *fbo = reinterpret_cast<uint32_t *>(kp.records_out + cand * (uint64_t)kp.stride + kp.off_fb);
             for (uint32_t w = 0; w < kp.fbw; w++) fbo[w * P + r] = 0u;
         }
-        if (MODE == 0 && laneOn) {
+        if (MODE != 1 && laneOn) {
             const uint32_t lim = 2 * n;
             uint32_t ones = 0;
             for (uint32_t w = 0; w < kp.fbw; w++) {
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         uint64_t tlast = 0, busy = 0;
         uint32_t cur = 0, peak = 0;
         const uint32_t S2 = 2 * n;
-        if (MODE == 0) {
+        if (MODE != 1) {   // MODE 0: score; MODE 2: score and record every stage's start/end
         // ---------------- K3: lock-step wavefront longest path ----------------
         // Per round every lane of the group tries its next slot (F if bit t is 0, else B):
         // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
@@ -383,6 +383,11 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 const uint64_t st = dep > tlast ? dep : tlast;
                 const uint64_t end = st + lat;
                 tlast = end;
+                if (MODE == 2) {
+                    const uint64_t o = (cand * P + r) * (uint64_t)(2 * n_max) + t;
+                    kp.tl_start[o] = st;
+                    kp.tl_end[o] = end;
+                }
                 busy += lat;
                 cur = d ? cur - act : cur + act;
                 peak = cur > peak ? cur : peak;
@@ -626,6 +631,7 @@ __global__ void make_gkey(const unsigned long long *key, unsigned long long *gke
 template <int G>
 static cudaError_t launch_g(const KParams &kp, int grid, int block, size_t smem, cudaStream_t s) {
     if (kp.records_out) dip_eval_kernel<G, 1><<<grid, block, smem, s>>>(kp);
+    else if (kp.tl_start) dip_eval_kernel<G, 2><<<grid, block, smem, s>>>(kp);
     else dip_eval_kernel<G, 0><<<grid, block, smem, s>>>(kp);
     return cudaGetLastError();
 }
@@ -643,21 +649,25 @@ cudaError_t launch_eval(const KParams &kp, int G, int grid, int block, size_t sm
 template <int G, int MODE>
 static const void *kfun() { return reinterpret_cast<const void *>(&dip_eval_kernel<G, MODE>); }
 static const void *kernel_for(int G, int mode) {
-    switch (G * 2 + mode) {
-    case 8: return kfun<4, 0>();
-    case 9: return kfun<4, 1>();
-    case 16: return kfun<8, 0>();
-    case 17: return kfun<8, 1>();
-    case 32: return kfun<16, 0>();
-    case 33: return kfun<16, 1>();
-    case 64: return kfun<32, 0>();
-    case 65: return kfun<32, 1>();
+    switch (G * 4 + mode) {
+    case 16: return kfun<4, 0>();
+    case 17: return kfun<4, 1>();
+    case 18: return kfun<4, 2>();
+    case 32: return kfun<8, 0>();
+    case 33: return kfun<8, 1>();
+    case 34: return kfun<8, 2>();
+    case 64: return kfun<16, 0>();
+    case 65: return kfun<16, 1>();
+    case 66: return kfun<16, 2>();
+    case 128: return kfun<32, 0>();
+    case 129: return kfun<32, 1>();
+    case 130: return kfun<32, 2>();
     default: return nullptr;
     }
 }
 
 cudaError_t prepare_eval(int G, size_t smem) {
-    for (int mode = 0; mode < 2; mode++) {
+    for (int mode = 0; mode < 3; mode++) {
         const void *f = kernel_for(G, mode);
         if (!f) return cudaErrorInvalidValue;
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

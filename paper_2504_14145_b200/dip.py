@@ -50,6 +50,24 @@ class _CandBatch(ctypes.Structure):
                 ("bwd_seq", ctypes.c_void_p), ("fb_bits", ctypes.c_void_p)]
 
 
+class _SearchParams(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("rounds", ctypes.c_uint32), ("leaves", ctypes.c_uint32),
+                ("rollouts", ctypes.c_uint32), ("threads", ctypes.c_int32), ("alpha", ctypes.c_double),
+                ("beta", ctypes.c_double)]
+
+
+class _SearchResult(ctypes.Structure):
+    _fields_ = [("found", ctypes.c_int32), ("rounds_done", ctypes.c_uint32), ("makespan_ns", ctypes.c_uint64),
+                ("score", ctypes.c_double), ("rollouts_scored", ctypes.c_uint64), ("tree_nodes", ctypes.c_uint64)]
+
+
+class _Action(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("kind", "peer", "tag", "batch", "slot")]
+
+
+ACTION_NAMES = ["fw_stage", "bw_stage", "isend", "irecv", "wait_isend", "wait_irecv"]
+
+
 class _Winner(ctypes.Structure):
     _fields_ = [("found", ctypes.c_int32), ("rank", ctypes.c_int32), ("global_index", ctypes.c_uint64),
                 ("makespan_ns", ctypes.c_uint64)]
@@ -85,6 +103,7 @@ def lib():
     L.dip_workspace_free.argtypes = [vp]
     L.dip_eval_schedules.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
     L.dip_interleave.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
+    L.dip_search.argtypes = [vp, vp, vp, ctypes.POINTER(_SearchParams), vp, vp, ctypes.POINTER(_SearchResult), vp]
     L.dip_argmin.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp,
                              ctypes.POINTER(_Winner), vp]
     L.dip_eval_host.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
@@ -92,13 +111,18 @@ def lib():
     L.dip_pack_key.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                ctypes.POINTER(ctypes.c_uint64)]
     L.dip_unpack_key.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_Winner)]
+    L.dip_timeline.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    L.dip_compile_plan.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(ctypes.c_uint32)]
+    L.dip_validate_plan.argtypes = [vp, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_int32)]
     L.dip_comm_unique_id.argtypes = [vp]
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
     for f in ("dip_load_cost_model", "dip_model_free", "dip_model_get_info", "dip_encode_candidates",
-              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_interleave", "dip_argmin",
+              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_interleave", "dip_search",
+              "dip_argmin",
               "dip_eval_host",
-              "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key"):
+              "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key",
+              "dip_timeline", "dip_compile_plan", "dip_validate_plan"):
         getattr(L, f).restype = st
     L.dip_launch_count.restype = ctypes.c_uint64
     L.dip_launch_count.argtypes = []
@@ -258,6 +282,59 @@ def interleave(model: Model, ws: Workspace, d_records, count: int, d_results, d_
     and score it (results as eval_schedules)."""
     _check(lib().dip_interleave(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results),
                                 _ptr(d_peaks), _stream(stream)), "dip_interleave")
+
+
+def search(model: Model, ws: Workspace, split, seed: int, rounds: int, leaves: int, rollouts: int,
+           alpha: float = 1.0, beta: float = 0.5, threads: int = 0, stream=None) -> dict:
+    """f2: MCTS over class orders for a fixed split with batched GPU rollouts.
+    Returns dict(found, makespan, score, trace, record (host bytes of the best schedule), ...)."""
+    sp = np.ascontiguousarray(np.asarray(split, np.uint8).reshape(-1))
+    prm = _SearchParams(seed & ((1 << 64) - 1), rounds, leaves, rollouts, threads, alpha, beta)
+    out = _SearchResult()
+    rec = np.zeros(model.stride, np.uint8)
+    trace = np.zeros(rounds, np.float64)
+    _check(lib().dip_search(model.handle, ws.handle, sp.ctypes.data, ctypes.byref(prm), rec.ctypes.data,
+                            trace.ctypes.data, ctypes.byref(out), _stream(stream)), "dip_search")
+    return dict(found=bool(out.found), makespan=out.makespan_ns, score=out.score, trace=trace, record=rec,
+                rounds_done=out.rounds_done, scored=out.rollouts_scored, tree_nodes=out.tree_nodes)
+
+
+def timeline(model: Model, ws: Workspace, d_records, count: int, d_results, d_start, d_end, stream=None):
+    """eval_schedules + per-slot start / end times ([count][P][2*n_max] u64 device buffers)."""
+    _check(lib().dip_timeline(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results), _ptr(d_start),
+                              _ptr(d_end), _stream(stream)), "dip_timeline")
+
+
+def compile_plan(model: Model, record, start, end):
+    """f4 (P:717-734): per-rank action lists of one schedule. record: host uint8[stride];
+    start / end: host uint64 [P, 2*n_max]. Returns (actions structured array, rank_off, n_messages)."""
+    rec = np.ascontiguousarray(record, np.uint8)
+    st = np.ascontiguousarray(start, np.uint64)
+    en = np.ascontiguousarray(end, np.uint64)
+    off = np.zeros(model.P + 1, np.uint32)
+    nmsg = ctypes.c_uint32()
+    cap = 1 << 16
+    while True:
+        acts = np.zeros((cap, 5), np.uint32)
+        code = lib().dip_compile_plan(model.handle, rec.ctypes.data, st.ctypes.data, en.ctypes.data,
+                                      acts.ctypes.data, cap, off.ctypes.data, ctypes.byref(nmsg))
+        if code == 4 and off[-1] > cap:   # DIP_ERANGE: grow
+            cap = int(off[-1])
+            continue
+        _check(code, "dip_compile_plan")
+        return acts[: off[-1]], off, nmsg.value
+
+
+def validate_plan(model: Model, record, acts, off):
+    """Discrete-event execution of a plan -> (ok, stage start times [P, 2*n_max])."""
+    rec = np.ascontiguousarray(record, np.uint8)
+    a = np.ascontiguousarray(acts, np.uint32)
+    o = np.ascontiguousarray(off, np.uint32)
+    st = np.zeros((model.P, 2 * model.n_max), np.uint64)
+    ok = ctypes.c_int32()
+    _check(lib().dip_validate_plan(model.handle, rec.ctypes.data, a.ctypes.data, o.ctypes.data, st.ctypes.data,
+                                   ctypes.byref(ok)), "dip_validate_plan")
+    return bool(ok.value), st
 
 
 def argmin(model: Model, ws: Workspace, count: int, shard_stride: Optional[int] = None, rank: int = 0,

@@ -1,0 +1,119 @@
+"""Pins of the oracle's MCTS segment reordering (S1-S6, §5.1).
+
+* exhaustive budget on a tiny instance -> the brute-force optimum over every class order
+  ("exhaustive budget -> ... equal to brute force"), the brute force built here with an
+  independent priority -> queue-order builder and the (pinned) oracle interleaving;
+* the best-so-far trace never decreases;
+* the reported best schedule re-scores to the reported makespan with the fixed-order oracle;
+* determinism for a seed.
+"""
+import itertools
+
+import numpy as np
+
+import gen
+import oracle
+from gen import Candidates, Module, Problem
+from tests import helpers as H
+
+
+def tiny_problem():
+    # one module, P = 2, three microbatches of different work (so the order matters)
+    md = Module("m", 2, 1, 1, 4, 0, *H.table(4, {1: (3, 6, 1, 0), 2: (5, 10, 2, 1), 4: (9, 18, 4, 1)}))
+    off = np.arange(4, dtype=np.uint32)
+    units = np.array([1, 4, 2], np.uint16)
+    return Problem("tiny", 2, 3, [md], off, units, np.full(2, 1 << 20, np.uint32))
+
+
+def orders_from_sequence(pb, split, seq):
+    """Independent builder of S2: class priorities -> forward / backward queue orders."""
+    nm = pb.nmod
+    base = pb.seg_base()
+    classes = [q for q in range(pb.m * nm) if split[q]]
+    C = len(classes)
+    Cn = 2 * C
+    prio = {c: Cn - 1 - p for p, c in enumerate(seq)}
+    segs = []
+    for q in classes:
+        b, i = divmod(q, nm)
+        for j in range(int(split[q])):
+            for k in range(pb.modules[i].K):
+                segs.append((b, i, j, k, int(base[b, i]) + j * pb.modules[i].K + k))
+    out = []
+    for d in (0, 1):
+        done = set()
+        order = []
+        while len(order) < len(segs):
+            ready = []
+            for (b, i, j, k, s) in segs:
+                if s in done:
+                    continue
+                K = pb.modules[i].K
+                if d == 0:
+                    preds = [s - 1] if k > 0 else [int(base[b, p]) + jj * pb.modules[p].K + pb.modules[p].K - 1
+                                                   for p in range(nm) if (pb.modules[i].producer_mask >> p) & 1
+                                                   for jj in range(int(split[b * nm + p]))]
+                else:
+                    preds = [s + 1] if k + 1 < K else [int(base[b, c]) + jj * pb.modules[c].K
+                                                       for c in range(nm) if (pb.modules[c].producer_mask >> i) & 1
+                                                       for jj in range(int(split[b * nm + c]))]
+                if all(p in done for p in preds):
+                    cls = classes.index(b * nm + i) + (C if d else 0)
+                    ready.append(((Cn - 1 - prio[cls]), j, (K - 1 - k) if d else k, s))
+            pick = min(ready)[3]
+            done.add(pick)
+            order.append(pick)
+        out.append(order)
+    return out
+
+
+def brute_force(pb, split):
+    nm = pb.nmod
+    C = sum(1 for q in range(pb.m * nm) if split[q])
+    perms = list(itertools.permutations(range(2 * C)))
+    cs = Candidates(pb, len(perms))
+    n = sum(int(split[q]) * pb.modules[q % nm].K for q in range(pb.m * nm))
+    for x, seq in enumerate(perms):
+        f, b = orders_from_sequence(pb, split, seq)
+        cs.split[x] = split
+        cs.n[x] = n
+        cs.fwd[x, :n] = f
+        cs.bwd[x, :n] = b
+    bits, r = oracle.interleave(pb, cs, threads=8)
+    LB = max(sum(int(pb.modules[0].f_ns[u]) + int(pb.modules[0].b_ns[u]) for u in pb.inst_units) for _ in range(pb.P))
+    ok = r.status == oracle.ST_OK
+    return max(LB / float(mk) for mk in r.makespan[ok]), int(r.makespan[ok].min())
+
+
+def test_exhaustive_budget_finds_brute_force_optimum():
+    pb = tiny_problem()
+    split = np.ones(3, np.uint8)
+    best_score, best_mk = brute_force(pb, split)
+    r = oracle.search(pb, split, seed=11, rounds=150, leaves=2, rollouts=10)
+    assert r["makespan"] == best_mk
+    assert abs(r["score"] - best_score) == 0.0
+
+
+def test_trace_monotone_and_best_record_rescores():
+    pb = gen.make_problem("12B")
+    cs = gen.generate(pb, 0, 1, p_mutate=0, p_bad=0)
+    r = oracle.search(pb, cs.split[0], seed=3, rounds=12, leaves=4, rollouts=6)
+    tr = r["trace"]
+    assert (np.diff(tr) >= 0).all() and tr[-1] == r["score"] > 0
+    c = cs.subset([0])
+    n = int(c.n[0])
+    c.fwd[0] = r["fwd"]
+    c.bwd[0] = r["bwd"]
+    c.fb[0] = r["bits"]
+    rr = oracle.evaluate(pb, c)
+    assert rr.status[0] == oracle.ST_OK and int(rr.makespan[0]) == r["makespan"]
+    assert sorted(r["fwd"][:n].tolist()) == sorted(cs.fwd[0][:n].tolist())
+
+
+def test_search_is_deterministic_per_seed():
+    pb = gen.make_problem("toy")
+    cs = gen.generate(pb, 0, 1, mode=1)
+    a = oracle.search(pb, cs.split[0], seed=5, rounds=10, leaves=3, rollouts=4)
+    b = oracle.search(pb, cs.split[0], seed=5, rounds=10, leaves=3, rollouts=4)
+    assert np.array_equal(a["trace"], b["trace"]) and a["makespan"] == b["makespan"]
+    assert np.array_equal(a["bits"], b["bits"])
