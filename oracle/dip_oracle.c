@@ -848,6 +848,7 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
         if (trace) trace[rd] = best;
     }
     *best_score = best > 0.0 ? best : 0.0;
+    if (!(best > 0.0)) *best_makespan = UINT64_MAX;     /* no feasible (status OK) rollout */
     for (uint32_t x = 0; x < nn; x++) free(T[x].ch);
     free(T); free(spl); free(nn_); free(fw); free(bw); free(fb); free(bits); free(owner); free(leaf);
     free(seq); free(prio); free(rest); free(used); free(base); free(clsof);
