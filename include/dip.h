@@ -168,8 +168,9 @@ dip_status dip_interleave(const dip_model *m, dip_workspace *w, void *d_records,
                           dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
 
 /* DIP's MCTS segment reordering (§5.1) with batched
- * GPU rollouts. For the given split, classes = (direction, microbatch, module) with M > 0 (one
- * priority per modality per microbatch, fixed internal order); a sequence of classes
+ * GPU rollouts. For the given split, classes = (direction, microbatch, module, chunk k) with M > 0
+ * (one priority per modality, microbatch and chunk; its M sub-microbatch segments keep a fixed
+ * order, R-32); a sequence of classes
  * gives priorities (position p -> Cn-1-p) -> forward / backward priority orders -> f1
  * interleaving -> score LB / makespan (0 if not OK; LB = busiest rank's total latency). Each
  * round selects `leaves` leaves by UCB s^alpha + beta*sqrt(ln N_parent / N_child) with

@@ -620,12 +620,13 @@ int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint
 /* ======================================================================================
  * S1-S6: DIP's MCTS segment reordering (§5.1), the row f2 of SURVEY §8(f),
  * written step by step from the paper with the readings of DESIGN.md §3 (R-32..R-35):
- *   S1 classes: (direction, microbatch b, module i) with M_{b,i} > 0 -- same-modality segments of
- *      one microbatch share a priority and keep a fixed order; forward classes in
- *      (b, i) order, then the backward classes in the same order.
+ *   S1 classes: (direction, microbatch b, module i, chunk k) with M_{b,i} > 0 -- the M_{b,i}
+ *      sub-microbatch segments of one modality, microbatch and chunk share a priority and keep a
+ *      fixed order, j ascending (reading R-32); forward classes in (b, i, k) order, then
+ *      the backward classes in the same order.
  *   S2 a sequence (permutation of the Cn classes) gives priority Cn-1-p to the class at position p
  *      (P:481); the forward / backward queue order of a rank = repeatedly the ready segment of the
- *      highest priority (within a class: j ascending, k ascending for F / descending for B).
+ *      highest priority (within a class: j ascending).
  *   S3 rollout score: interleave (I1-I6) and score LB / makespan if OK, else 0, with LB the
  *      busiest rank's summed latency of the split.
  *   S4 selection: from the root, while the node has all its children, move to the child of
@@ -673,8 +674,8 @@ static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *ba
                         else for (uint32_t c = 0; c < nm; c++) if ((pb->producer_mask[c] >> i) & 1u) d += split[b * nm + c];
                     }
                     indeg[s] = d;
-                    uint32_t c = (uint32_t)clsof[q] + (dir ? C : 0);
-                    key[s] = ((uint64_t)(Cn - 1 - prio[c]) << 40) | ((uint64_t)j << 24) | ((uint64_t)(dir ? K - 1 - k : k) << 12);
+                    uint32_t c = (uint32_t)clsof[q] + k + (dir ? C : 0);
+                    key[s] = ((uint64_t)(Cn - 1 - prio[c]) << 40) | ((uint64_t)j << 24);
                     if (d == 0) ready[s] = 1;
                     n++;
                 }
@@ -722,7 +723,8 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
     for (uint32_t q = 0; q < m * nm; q++) {
         base[q] = acc;
         acc += pb->max_split[q % nm] * pb->K[q % nm];
-        clsof[q] = split[q] ? (int)C++ : -1;
+        clsof[q] = split[q] ? (int)C : -1;                   /* classes (b, i, 0..K_i-1) */
+        if (split[q]) C += pb->K[q % nm];
         n += split[q] * pb->K[q % nm];
     }
     const uint32_t Cn = 2 * C;

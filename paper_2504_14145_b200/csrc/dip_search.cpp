@@ -1,12 +1,12 @@
 // dip_search.cpp -- SURVEY §8(f) row f2: DIP's MCTS segment reordering (§5.1)
 // driving batched GPU rollouts (each rollout = priorities -> dual-queue interleaving (f1) -> score).
 //
-// Search space: for a fixed split, the classes are (direction, microbatch b,
-// module i) with M_{b,i} > 0 -- segments of one modality within one microbatch share a priority
-// and keep a fixed internal order -- and a sequence is a permutation of all classes; the class at
-// position p gets priority Cn - 1 - p. A forward (backward) priority order is the highest-priority
-// ready segment first over the forward (backward) segment DAG (within a class: j ascending, k
-// ascending for F / descending for B), so it is always a linear extension.
+// Search space (reading R-32): for a fixed split, the classes are (direction,
+// microbatch b, module i, chunk k) with M_{b,i} > 0 -- the sub-microbatch segments of one modality,
+// microbatch and chunk share a priority and keep a fixed internal order (j ascending) -- and a
+// sequence is a permutation of all classes; the class at position p gets priority Cn - 1 - p. A
+// forward (backward) priority order is the highest-priority ready segment first over the forward
+// (backward) segment DAG, so it is always a linear extension.
 // Tree: node at depth d fixes the class of position d; s_v = best score below v,
 // N_v = visits. Selection: UCB s_v^alpha + beta * sqrt(ln N_x / N_v), ties to the lowest
 // class; expansion: the next child in class order; rollouts: uniformly random
@@ -51,8 +51,8 @@ struct Node {
 struct Setup {
     uint32_t P, nm, m, n, C, Cn;
     std::vector<uint8_t> M;            // [m*nm]
-    std::vector<int> cls_of;           // [m*nm] -> class index of (b,i) (forward), -1 if absent
-    std::vector<uint32_t> cls_q;       // class (0..C-1) -> (b*nm + i)
+    std::vector<int> cls_of;           // [m*nm] -> class index of (b,i,k=0) (forward), -1 if absent
+    std::vector<uint32_t> cls_q;       // present (b*nm + i), in class order
     std::vector<uint32_t> q_of_seg;    // segment id -> (b*nm + i)
     double LB;
 };
@@ -65,10 +65,10 @@ void order(const dip_model *Md, const Setup &S, const std::vector<uint32_t> &pri
     typedef std::pair<uint64_t, uint32_t> E;
     std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
     auto key = [&](uint32_t b, uint32_t i, uint32_t j, uint32_t k, uint32_t K) -> uint64_t {
-        const uint32_t c = (uint32_t)S.cls_of[b * nm + i] + (dir ? S.C : 0);
+        (void)K;
+        const uint32_t c = (uint32_t)S.cls_of[b * nm + i] + k + (dir ? S.C : 0);
         const uint64_t rank = (uint64_t)(S.Cn - 1 - prio[c]);                 // higher priority first
-        const uint64_t kk = dir ? (K - 1 - k) : k;
-        return (rank << 40) | ((uint64_t)j << 24) | (kk << 12);
+        return (rank << 40) | ((uint64_t)j << 24);
     };
     for (uint32_t b = 0; b < S.m; b++)
         for (uint32_t i = 0; i < nm; i++) {
@@ -147,14 +147,14 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     S.M.assign(split, split + S.m * S.nm);
     S.cls_of.assign(S.m * S.nm, -1);
     S.n = 0;
+    S.C = 0;
     for (uint32_t b = 0; b < S.m; b++)
         for (uint32_t i = 0; i < S.nm; i++) {
             const uint32_t q = b * S.nm + i, N = Md->nbi[q], Mv = S.M[q];
             if ((N == 0) != (Mv == 0) || Mv > std::min(N, Md->max_split[i])) return fail(DIP_EINVAL, "invalid split");
-            if (Mv) { S.cls_of[q] = (int)S.cls_q.size(); S.cls_q.push_back(q); }
+            if (Mv) { S.cls_of[q] = (int)S.C; S.C += Md->Kv[i]; S.cls_q.push_back(q); }
             S.n += Mv * Md->Kv[i];
         }
-    S.C = (uint32_t)S.cls_q.size();
     S.q_of_seg.assign(Md->n_max, 0);
     for (uint32_t q = 0; q < S.m * S.nm; q++)
         for (uint32_t x = 0; x < Md->max_split[q % S.nm] * Md->Kv[q % S.nm]; x++) S.q_of_seg[Md->sbase[q] + x] = q;

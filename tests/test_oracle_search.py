@@ -29,16 +29,15 @@ def orders_from_sequence(pb, split, seq):
     """Independent builder of S2: class priorities -> forward / backward queue orders."""
     nm = pb.nmod
     base = pb.seg_base()
-    classes = [q for q in range(pb.m * nm) if split[q]]
+    classes = [(q, k) for q in range(pb.m * nm) if split[q] for k in range(pb.modules[q % nm].K)]
     C = len(classes)
     Cn = 2 * C
     prio = {c: Cn - 1 - p for p, c in enumerate(seq)}
     segs = []
-    for q in classes:
+    for q, k in classes:
         b, i = divmod(q, nm)
         for j in range(int(split[q])):
-            for k in range(pb.modules[i].K):
-                segs.append((b, i, j, k, int(base[b, i]) + j * pb.modules[i].K + k))
+            segs.append((b, i, j, k, int(base[b, i]) + j * pb.modules[i].K + k))
     out = []
     for d in (0, 1):
         done = set()
@@ -58,9 +57,9 @@ def orders_from_sequence(pb, split, seq):
                                                        for c in range(nm) if (pb.modules[c].producer_mask >> i) & 1
                                                        for jj in range(int(split[b * nm + c]))]
                 if all(p in done for p in preds):
-                    cls = classes.index(b * nm + i) + (C if d else 0)
-                    ready.append(((Cn - 1 - prio[cls]), j, (K - 1 - k) if d else k, s))
-            pick = min(ready)[3]
+                    cls = classes.index((b * nm + i, k)) + (C if d else 0)
+                    ready.append(((Cn - 1 - prio[cls]), j, s))
+            pick = min(ready)[2]
             done.add(pick)
             order.append(pick)
         out.append(order)
@@ -69,7 +68,7 @@ def orders_from_sequence(pb, split, seq):
 
 def brute_force(pb, split):
     nm = pb.nmod
-    C = sum(1 for q in range(pb.m * nm) if split[q])
+    C = sum(pb.modules[q % nm].K for q in range(pb.m * nm) if split[q])
     perms = list(itertools.permutations(range(2 * C)))
     cs = Candidates(pb, len(perms))
     n = sum(int(split[q]) * pb.modules[q % nm].K for q in range(pb.m * nm))
@@ -80,7 +79,8 @@ def brute_force(pb, split):
         cs.fwd[x, :n] = f
         cs.bwd[x, :n] = b
     bits, r = oracle.interleave(pb, cs, threads=8)
-    LB = max(sum(int(pb.modules[0].f_ns[u]) + int(pb.modules[0].b_ns[u]) for u in pb.inst_units) for _ in range(pb.P))
+    md = pb.modules[0]                       # one module, L divisible by P: L / P layers per rank
+    LB = (md.L // pb.P) * sum(int(md.f_ns[u]) + int(md.b_ns[u]) for u in pb.inst_units)
     ok = r.status == oracle.ST_OK
     return max(LB / float(mk) for mk in r.makespan[ok]), int(r.makespan[ok].min())
 
@@ -117,3 +117,16 @@ def test_search_is_deterministic_per_seed():
     b = oracle.search(pb, cs.split[0], seed=5, rounds=10, leaves=3, rollouts=4)
     assert np.array_equal(a["trace"], b["trace"]) and a["makespan"] == b["makespan"]
     assert np.array_equal(a["bits"], b["bits"])
+
+
+def test_exhaustive_budget_with_chunk_classes():
+    # K = 2 chunks per segment: each (microbatch, chunk) is its own class (R-32), so an
+    # interleaved-VPP-like order (chunk 0 of both microbatches before chunk 1) is reachable
+    md = Module("m", 4, 2, 1, 4, 0, *H.table(4, {1: (3, 6, 1, 0), 3: (7, 14, 3, 1)}))
+    pb = Problem("tiny2", 2, 2, [md], np.arange(3, dtype=np.uint32), np.array([1, 3], np.uint16),
+                 np.full(2, 1 << 20, np.uint32))
+    split = np.ones(2, np.uint8)
+    best_score, best_mk = brute_force(pb, split)
+    r = oracle.search(pb, split, seed=2, rounds=1200, leaves=100, rollouts=2)
+    assert r["makespan"] == best_mk
+    assert abs(r["score"] - best_score) == 0.0
