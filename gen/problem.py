@@ -406,3 +406,34 @@ def problem_arrays(pb: Problem):
     chunk = np.concatenate(cl).astype(np.uint32) if cl else np.zeros(0, np.uint32)
     return dict(L=L, K=K, max_split=ms, w_max=wm, producer_mask=pm, tab_off=toff,
                 tab_f=tf, tab_b=tb, tab_act=ta, tab_p2p=tp, chunk_off=coff, chunk_layers=chunk)
+
+
+# ---------------------------------------------------------------------------
+# Per-layer memory-strategy menu (f3, §5.3; R-37)
+# ---------------------------------------------------------------------------
+N_STRAT = 3
+# strategy c: backward latency saved (in units of the layer's forward latency) and activation
+# growth factor, relative to the base tables (strategy 0 = the most memory-efficient scheme,
+# the one every other row uses): 0 keeps the base recomputation, 1 keeps the MLP
+# activations (no MLP recompute), 2 keeps everything (no recompute at all).
+STRAT_SAVE = ((0, 1), (1, 4), (2, 5))        # fraction num/den of F saved in B
+STRAT_GROW = ((1, 1), (3, 2), (9, 4))        # activation x num/den
+
+
+def strategy_menu(pb: Problem):
+    """(f, b, act) uint32 arrays [N_STRAT, T] aligned with problem_arrays' tables (T = sum of
+    w_max_i + 1): per-layer F ns, B ns and activation KiB of each strategy. Input data only."""
+    a = problem_arrays(pb)
+    T = len(a["tab_f"])
+    f = np.zeros((N_STRAT, T), np.uint32)
+    b = np.zeros((N_STRAT, T), np.uint32)
+    act = np.zeros((N_STRAT, T), np.uint32)
+    tf = a["tab_f"].astype(np.uint64)
+    tb = a["tab_b"].astype(np.uint64)
+    ta = a["tab_act"].astype(np.uint64)
+    for c in range(N_STRAT):
+        (sn, sd), (gn, gd) = STRAT_SAVE[c], STRAT_GROW[c]
+        f[c] = tf
+        b[c] = tb - (tf * sn) // sd
+        act[c] = (ta * gn + gd - 1) // gd
+    return f, b, act

@@ -68,6 +68,13 @@ def _load():
         lib.oracle_search.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
                                       ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                       ctypes.c_double, ctypes.c_double] + [ctypes.c_void_p] * 7
+        lib.oracle_mem_candidates.restype = ctypes.c_int
+        lib.oracle_mem_candidates.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 3 + [ctypes.c_uint32] * 2 + \
+            [ctypes.c_void_p]
+        lib.oracle_memopt.restype = ctypes.c_int
+        lib.oracle_memopt.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32] + [ctypes.c_void_p] * 3 + \
+            [ctypes.c_uint32, ctypes.POINTER(_OCands), ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 7 + \
+            [ctypes.c_int]
         lib.oracle_argmin.restype = ctypes.c_int64
         lib.oracle_argmin.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
         _lib = lib
@@ -183,6 +190,38 @@ def timeline(pb, cands, x: int):
     if status not in (ST_OK, ST_OOM):
         return status, None, None
     return status, st[:pb.P * 2 * n].reshape(pb.P, 2 * n), en[:pb.P * 2 * n].reshape(pb.P, 2 * n)
+
+
+def mem_candidates(f, b, act, layers: int, S: int):
+    """M2: the <= S (F ns, B ns, mem KiB) candidates of a stage pair of `layers`
+    identical layers whose per-layer strategy menu is (f[c], b[c], act[c]); sorted by memory."""
+    f = np.ascontiguousarray(f, np.uint32)
+    b = np.ascontiguousarray(b, np.uint32)
+    a = np.ascontiguousarray(act, np.uint32)
+    out = np.zeros((max(S, 2), 3), np.uint64)
+    k = _load().oracle_mem_candidates(len(f), f.ctypes.data, b.ctypes.data, a.ctypes.data, layers, S,
+                                      out.ctypes.data)
+    return [tuple(int(v) for v in out[x]) for x in range(k)]
+
+
+def memopt(pb, cands, menu, S: int = 10, first: int = 0, count: Optional[int] = None, threads: int = 1):
+    """M1-M4: per-layer memory optimisation of each candidate schedule. `menu` =
+    (f, b, act) arrays [n_strat, T] aligned with the model's tables. Returns (sel, Results) with
+    sel [count, P, 2, n_max] the selected candidate index of each pair at forward position p
+    (sel[..., 0, p]) and backward position q (sel[..., 1, q]) and the re-timed results."""
+    if count is None:
+        count = cands.count - first
+    f, b, a = (np.ascontiguousarray(v, np.uint32) for v in menu)
+    lib = _load()
+    bd = _Bound(pb, cands)
+    res = Results(count, pb.P)
+    sel = np.zeros((count, pb.P, 2, pb.n_max), np.uint8)
+    rc = lib.oracle_memopt(ctypes.byref(bd.pb), f.shape[0], f.ctypes.data, b.ctypes.data, a.ctypes.data, S,
+                           ctypes.byref(bd.cs), first, count, sel.ctypes.data, res.makespan.ctypes.data,
+                           res.status.ctypes.data, res.oom_mask.ctypes.data, res.bubble.ctypes.data,
+                           res.peaks.ctypes.data, res.busy.ctypes.data, threads)
+    assert rc == 0
+    return sel, res
 
 
 def argmin(makespan: np.ndarray, status: np.ndarray) -> int:

@@ -21,6 +21,7 @@
  *   O11 argmin             P:499-501 best score; ties -> lowest index (R-14, R-15)
  *   I1-I6 interleaving     P:511-548 the dual-queue greedy, see below
  *   S1-S6 search           P:472-509 MCTS segment reordering, see below
+ *   M1-M4 memory opt.      P:550-590 per-layer memory optimisation, see below
  *
  * Integers everywhere (ns, KiB); u64 accumulators.  The only floating-point
  * value, the bubble ratio, is one IEEE double division of two exact integers.
@@ -95,9 +96,11 @@ static uint32_t layers_of(const oproblem *pb, uint32_t i, uint32_t c) {
 }
 
 /* Evaluate candidate x.  peaks: [P] (u64), may be NULL.  If tl_start/tl_end are
- * given they receive per (rank, slot) start/end times ([P][2n]). */
+ * given they receive per (rank, slot) start/end times ([P][2n]).  If ovr is given
+ * ([P][idmax+1][3]: F latency, B latency, activation of each (rank, segment) stage pair), it
+ * replaces O6's table costs (M4 of the per-layer memory optimisation below). */
 static void eval_one(const oproblem *pb, const ocands *cs, uint64_t x, ores *res, uint64_t *peaks,
-                     uint64_t *tl_start, uint64_t *tl_end) {
+                     uint64_t *tl_start, uint64_t *tl_end, const uint64_t *ovr) {
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
     const uint32_t n_max = cs->n_max, fbw = cs->fbw;
     const uint8_t *split = cs->split + x * (uint64_t)m * nm;
@@ -202,6 +205,11 @@ static void eval_one(const oproblem *pb, const ocands *cs, uint64_t x, ores *res
                 uint64_t lay = layers_of(pb, i, k * P + r);
                 lat[node] = lay * (uint64_t)(isb ? pb->tab_b[toff] : pb->tab_f[toff]);
                 act[node] = lay * (uint64_t)pb->tab_act[toff];
+                if (ovr) {
+                    const uint64_t *o = ovr + ((uint64_t)r * (idmax + 1) + s) * 3;
+                    lat[node] = o[isb];
+                    act[node] = o[2];
+                }
             }
         }
         /* O7: explicit predecessor lists (dst node, src node, weight) */
@@ -322,7 +330,7 @@ static void *worker(void *arg) {
     for (uint64_t x = j->lo; x < j->hi; x++) {
         ores r;
         uint64_t o = x - j->first;
-        eval_one(j->pb, j->cs, x, &r, j->peaks ? j->peaks + o * j->pb->P : NULL, NULL, NULL);
+        eval_one(j->pb, j->cs, x, &r, j->peaks ? j->peaks + o * j->pb->P : NULL, NULL, NULL, NULL);
         j->makespan[o] = r.makespan;
         j->busy[o] = r.busy;
         j->status[o] = r.status;
@@ -356,7 +364,7 @@ int oracle_eval(const oproblem *pb, const ocands *cs, uint64_t first, uint64_t c
 /* Per-(rank, slot) start/end times of candidate x ([P][2n] each); returns the status. */
 int oracle_timeline(const oproblem *pb, const ocands *cs, uint64_t x, uint64_t *tl_start, uint64_t *tl_end) {
     ores r;
-    eval_one(pb, cs, x, &r, NULL, tl_start, tl_end);
+    eval_one(pb, cs, x, &r, NULL, tl_start, tl_end, NULL);
     return (int)r.status;
 }
 
@@ -863,4 +871,267 @@ int64_t oracle_argmin(const uint64_t *makespan, const uint32_t *status, uint64_t
     for (uint64_t x = 0; x < count; x++)
         if (status[x] == ST_OK && (best < 0 || makespan[x] < makespan[best])) best = (int64_t)x;
     return best;
+}
+
+/* ======================================================================================
+ * M1-M4: DIP's per-layer memory optimisation (§5.3), the row f3 of
+ * SURVEY §8(f), step by step with the readings of DESIGN.md §3 (R-37..R-40):
+ *   M1 menu: every layer of module i has n_strat strategies c with per-layer
+ *      (F ns, B ns, activation KiB) at width W -- an input, like the O6 tables; strategy 0 is
+ *      the scheme of the O6 tables (the "most memory-efficient scheme" the interleaving uses,
+ *      P:522-524).
+ *   M2 candidates of a stage pair: the pair = the forward stage and its backward
+ *      stage on one rank (chunk of `layers` identical layers at width W); a combination gives one
+ *      strategy to each layer (lat = sum F + B, mem = sum act). (1) the fastest combination,
+ *      (2) the most memory-efficient one, (3) the range [mem_min, mem_fast] cut evenly into S-2
+ *      buckets [lo_u, hi_u) and, in each, the fastest combination whose memory falls in it
+ *      (the multiple-choice knapsack optimum, written out as enumeration: the layers are
+ *      identical, so a combination is fixed by how many layers take each strategy). Ties: less
+ *      memory, then the smaller forward latency. Duplicates and dominated entries dropped;
+ *      sorted by memory ascending (so latency strictly decreases).
+ *   M3 selection on each rank: pairs i with interval [slot of F, slot of B) in
+ *      the rank's order; at every forward slot s_k the selected memory of the pairs live there
+ *      must stay <= the rank's budget M. The warm start ("greedy initial solution"):
+ *      start from candidate 0 everywhere (the min-memory one, feasible iff the schedule is not
+ *      OOM; if it is, nothing changes), then repeatedly move the pair with the largest
+ *      latency saving per KiB of extra memory (next candidate; ties: earliest forward slot) to
+ *      its next candidate as long as every point it covers keeps slack; the ILP refinement
+ *      with a <= 5 % gap is out of scope.
+ *   M4 score: the schedule re-timed (O7-O10) with every pair's selected latencies and
+ *      activations.
+ * ====================================================================================== */
+typedef struct { uint64_t f, b, mem; } mcand;
+
+static int mc_better(const mcand *a, const mcand *b, int by_mem) {   /* strict "a before b" */
+    uint64_t la = a->f + a->b, lb = b->f + b->b;
+    if (by_mem) {
+        if (a->mem != b->mem) return a->mem < b->mem;
+        if (la != lb) return la < lb;
+    } else {
+        if (la != lb) return la < lb;
+        if (a->mem != b->mem) return a->mem < b->mem;
+    }
+    return a->f < b->f;
+}
+
+/* M2: out [S][3] = (F ns, B ns, mem KiB) of the pair's candidates; returns their count. */
+int oracle_mem_candidates(uint32_t n_strat, const uint32_t *f, const uint32_t *b, const uint32_t *act,
+                          uint32_t layers, uint32_t S, uint64_t *out) {
+    if (n_strat == 0 || n_strat > 8 || S < 2 || layers == 0) return 0;
+    /* every count vector (n_0 .. n_{C-1}) with sum = layers */
+    uint32_t cnt[8] = {0}, ncomb = 0, cap = 64;
+    mcand *all = malloc(sizeof(mcand) * cap);
+    cnt[n_strat - 1] = 0;
+    for (;;) {
+        uint32_t used = 0;
+        for (uint32_t c = 0; c + 1 < n_strat; c++) used += cnt[c];
+        if (used <= layers) {
+            cnt[n_strat - 1] = layers - used;
+            mcand x = {0, 0, 0};
+            for (uint32_t c = 0; c < n_strat; c++) {
+                x.f += (uint64_t)cnt[c] * f[c];
+                x.b += (uint64_t)cnt[c] * b[c];
+                x.mem += (uint64_t)cnt[c] * act[c];
+            }
+            if (ncomb == cap) { cap *= 2; all = realloc(all, sizeof(mcand) * cap); }
+            all[ncomb++] = x;
+        }
+        /* next vector of the first n_strat-1 counts (odometer, each in [0, layers]) */
+        uint32_t c = 0;
+        while (c + 1 < n_strat) {
+            if (++cnt[c] <= layers) break;
+            cnt[c] = 0;
+            c++;
+        }
+        if (c + 1 >= n_strat) break;
+    }
+    mcand *pick = malloc(sizeof(mcand) * S);
+    uint32_t np = 0;
+    mcand fast = all[0], small = all[0];
+    for (uint32_t x = 1; x < ncomb; x++) {
+        if (mc_better(&all[x], &fast, 0)) fast = all[x];
+        if (mc_better(&all[x], &small, 1)) small = all[x];
+    }
+    pick[np++] = fast;
+    pick[np++] = small;
+    if (S > 2 && fast.mem > small.mem) {
+        uint64_t span = fast.mem - small.mem;
+        for (uint32_t u = 0; u < S - 2; u++) {
+            uint64_t lo = small.mem + span * u / (S - 2), hi = small.mem + span * (u + 1) / (S - 2);
+            int have = 0;
+            mcand best = {0, 0, 0};
+            for (uint32_t x = 0; x < ncomb; x++)
+                if (all[x].mem >= lo && all[x].mem < hi && (!have || mc_better(&all[x], &best, 0))) { best = all[x]; have = 1; }
+            if (have) pick[np++] = best;
+        }
+    }
+    /* drop duplicates and dominated entries, then sort by memory ascending */
+    uint32_t k = 0;
+    for (uint32_t x = 0; x < np; x++) {
+        int drop = 0;
+        for (uint32_t y = 0; y < np && !drop; y++) {
+            if (y == x) continue;
+            uint64_t lx = pick[x].f + pick[x].b, ly = pick[y].f + pick[y].b;
+            int same = pick[y].f == pick[x].f && pick[y].b == pick[x].b && pick[y].mem == pick[x].mem;
+            if (same && y < x) drop = 1;
+            if (!same && pick[y].mem <= pick[x].mem && ly <= lx && (pick[y].mem < pick[x].mem || ly < lx)) drop = 1;
+        }
+        if (!drop) pick[k++] = pick[x];
+    }
+    for (uint32_t x = 1; x < k; x++)
+        for (uint32_t y = x; y > 0 && pick[y].mem < pick[y - 1].mem; y--) { mcand t = pick[y]; pick[y] = pick[y - 1]; pick[y - 1] = t; }
+    for (uint32_t x = 0; x < k; x++) { out[3 * x] = pick[x].f; out[3 * x + 1] = pick[x].b; out[3 * x + 2] = pick[x].mem; }
+    free(all); free(pick);
+    return (int)k;
+}
+
+typedef struct {
+    uint32_t n_strat, S;
+    const uint32_t *f, *b, *act;    /* [n_strat][tab_off[nmod]] per-layer menu (M1) */
+} omenu;
+
+/* M2-M4 for candidate x: sel [P][2][n_max] (candidate index of the pair at forward position p /
+ * backward position q), then the re-timed result. */
+static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, uint64_t x, uint8_t *sel,
+                       ores *res, uint64_t *peaks) {
+    const uint32_t P = pb->P, nm = pb->nmod, m = pb->m, n_max = cs->n_max, fbw = cs->fbw;
+    const uint8_t *split = cs->split + x * (uint64_t)m * nm;
+    const uint16_t *fwd = cs->fwd + x * (uint64_t)n_max, *bwd = cs->bwd + x * (uint64_t)n_max;
+    const uint32_t *fb = cs->fb + x * (uint64_t)P * fbw;
+    const uint32_t n = cs->n[x], T = pb->tab_off[nm];
+    memset(sel, 0, (size_t)P * 2 * n_max);
+    ores r0;
+    eval_one(pb, cs, x, &r0, NULL, NULL, NULL, NULL);             /* encoding checks (O4) */
+    if (r0.status == ST_BAD || n == 0) { eval_one(pb, cs, x, res, peaks, NULL, NULL, NULL); return; }
+    uint32_t idmax = seg_count_max(pb);
+    uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
+    uint32_t *W = calloc(idmax + 1, sizeof(uint32_t)), *si = calloc(idmax + 1, sizeof(uint32_t)), *sk = calloc(idmax + 1, sizeof(uint32_t));
+    uint32_t acc = 0;
+    for (uint32_t b = 0; b < m; b++)
+        for (uint32_t i = 0; i < nm; i++) {
+            uint32_t q = b * nm + i;
+            base[q] = acc;
+            uint32_t lo = pb->inst_off[q], N = pb->inst_off[q + 1] - lo, M = split[q], st[16];
+            if (M) oracle_split(N, M, st);
+            for (uint32_t j = 0; j < pb->max_split[i]; j++)
+                for (uint32_t k = 0; k < pb->K[i]; k++) {
+                    uint32_t id = acc + j * pb->K[i] + k, w = 0;
+                    if (j < M) for (uint32_t u = st[j]; u < st[j + 1]; u++) w += pb->inst_units[lo + u];
+                    W[id] = w; si[id] = i; sk[id] = k;
+                }
+            acc += pb->max_split[i] * pb->K[i];
+        }
+    uint64_t *ovr = calloc((size_t)P * (idmax + 1) * 3, sizeof(uint64_t));
+    uint64_t *cl = malloc(sizeof(uint64_t) * 3 * mn->S * n);     /* candidates of each pair */
+    uint32_t *nc = malloc(sizeof(uint32_t) * n), *cur = malloc(sizeof(uint32_t) * n);
+    uint32_t *sF = malloc(sizeof(uint32_t) * n), *sB = malloc(sizeof(uint32_t) * n), *qpos = malloc(sizeof(uint32_t) * n);
+    int64_t *slack = malloc(sizeof(int64_t) * 2 * n);
+    uint32_t *fsl = malloc(sizeof(uint32_t) * n);                /* forward slots = the points s_k */
+    for (uint32_t r = 0; r < P; r++) {
+        /* the rank's order: slot of the p-th forward and of the q-th backward stage (O5) */
+        uint32_t fi = 0, bi = 0;
+        uint32_t *slotB_of_seg = malloc(sizeof(uint32_t) * (idmax + 1)), *qpos_of_seg = malloc(sizeof(uint32_t) * (idmax + 1));
+        for (uint32_t t = 0; t < 2 * n; t++) {
+            if ((fb[r * fbw + t / 32] >> (t % 32)) & 1u) { slotB_of_seg[bwd[bi]] = t; qpos_of_seg[bwd[bi]] = bi; bi++; }
+            else { sF[fi] = t; fsl[fi] = t; fi++; }
+        }
+        for (uint32_t p = 0; p < n; p++) {                          /* pair p = segment fwd[p] */
+            uint32_t s = fwd[p], i = si[s], lay = layers_of(pb, i, sk[s] * P + r), toff = pb->tab_off[i] + W[s];
+            uint32_t ff[8], bb[8], aa[8];
+            for (uint32_t c = 0; c < mn->n_strat; c++) {
+                ff[c] = mn->f[c * T + toff]; bb[c] = mn->b[c * T + toff]; aa[c] = mn->act[c * T + toff];
+            }
+            nc[p] = lay ? (uint32_t)oracle_mem_candidates(mn->n_strat, ff, bb, aa, lay, mn->S, cl + (size_t)3 * mn->S * p) : 0;
+            if (nc[p] == 0) { nc[p] = 1; cl[(size_t)3 * mn->S * p] = 0; cl[(size_t)3 * mn->S * p + 1] = 0; cl[(size_t)3 * mn->S * p + 2] = 0; }
+            cur[p] = 0;
+            sB[p] = slotB_of_seg[s];
+            qpos[p] = qpos_of_seg[s];
+        }
+        /* M3: slack at every forward slot with candidate 0 everywhere */
+        int feasible = 1;
+        for (uint32_t k = 0; k < n; k++) {
+            int64_t used = 0;
+            for (uint32_t p = 0; p < n; p++)
+                if (sF[p] <= fsl[k] && fsl[k] < sB[p]) used += (int64_t)cl[(size_t)3 * mn->S * p + 2];
+            slack[k] = (int64_t)pb->budget_kib[r] - used;
+            if (slack[k] < 0) feasible = 0;
+        }
+        while (feasible) {
+            int best = -1;
+            uint64_t bl = 0, bm = 1;
+            for (uint32_t p = 0; p < n; p++) {
+                if (cur[p] + 1 >= nc[p]) continue;
+                const uint64_t *a = cl + (size_t)3 * mn->S * p + 3 * cur[p];
+                uint64_t dl = (a[0] + a[1]) - (a[3] + a[4]), dm = a[5] - a[2];
+                int ok = 1;
+                for (uint32_t k = 0; k < n && ok; k++)
+                    if (sF[p] <= fsl[k] && fsl[k] < sB[p] && slack[k] < (int64_t)dm) ok = 0;
+                if (!ok) continue;
+                /* dl/dm > bl/bm, exactly; ties keep the earlier forward slot (lower p) */
+                if (best < 0 || (unsigned __int128)dl * bm > (unsigned __int128)bl * dm) { best = (int)p; bl = dl; bm = dm; }
+            }
+            if (best < 0) break;
+            for (uint32_t k = 0; k < n; k++)
+                if (sF[best] <= fsl[k] && fsl[k] < sB[best]) slack[k] -= (int64_t)bm;
+            cur[best]++;
+        }
+        for (uint32_t p = 0; p < n; p++) {
+            const uint64_t *a = cl + (size_t)3 * mn->S * p + 3 * cur[p];
+            uint64_t *o = ovr + ((uint64_t)r * (idmax + 1) + fwd[p]) * 3;
+            o[0] = a[0]; o[1] = a[1]; o[2] = a[2];
+            sel[((size_t)r * 2 + 0) * n_max + p] = (uint8_t)cur[p];
+            sel[((size_t)r * 2 + 1) * n_max + qpos[p]] = (uint8_t)cur[p];
+        }
+        free(slotB_of_seg); free(qpos_of_seg);
+    }
+    eval_one(pb, cs, x, res, peaks, NULL, NULL, ovr);          /* M4 */
+    free(base); free(W); free(si); free(sk); free(ovr); free(cl); free(nc); free(cur);
+    free(sF); free(sB); free(qpos); free(slack); free(fsl);
+}
+
+typedef struct {
+    const oproblem *pb;
+    const omenu *mn;
+    const ocands *cs;
+    uint64_t lo, hi, first;
+    uint8_t *sel;
+    uint64_t *makespan, *busy, *peaks;
+    uint32_t *status, *oom;
+    double *bubble;
+} mjob_t;
+
+static void *mworker(void *arg) {
+    mjob_t *j = (mjob_t *)arg;
+    const uint32_t P = j->pb->P;
+    for (uint64_t x = j->lo; x < j->hi; x++) {
+        ores r;
+        uint64_t o = x - j->first;
+        memopt_one(j->pb, j->mn, j->cs, x, j->sel + o * (uint64_t)P * 2 * j->cs->n_max, &r, j->peaks ? j->peaks + o * P : NULL);
+        j->makespan[o] = r.makespan; j->busy[o] = r.busy; j->status[o] = r.status;
+        j->oom[o] = r.oom_mask; j->bubble[o] = r.bubble;
+    }
+    return NULL;
+}
+
+int oracle_memopt(const oproblem *pb, uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma,
+                  uint32_t S, const ocands *cs, uint64_t first, uint64_t count, uint8_t *sel /* [count][P][2][n_max] */,
+                  uint64_t *makespan, uint32_t *status, uint32_t *oom_mask, double *bubble, uint64_t *peaks,
+                  uint64_t *busy, int threads) {
+    if (n_strat == 0 || n_strat > 8 || S < 2 || S > 16) return -1;
+    omenu mn = {n_strat, S, mf, mb, ma};
+    if (threads < 1) threads = 1;
+    if (threads > 512) threads = 512;
+    if ((uint64_t)threads > count) threads = count ? (int)count : 1;
+    pthread_t th[512];
+    mjob_t jobs[512];
+    uint64_t per = (count + threads - 1) / threads;
+    for (int t = 0; t < threads; t++) {
+        uint64_t lo = first + per * t, hi = lo + per;
+        if (hi > first + count) hi = first + count;
+        if (lo > hi) lo = hi;
+        jobs[t] = (mjob_t){pb, &mn, cs, lo, hi, first, sel, makespan, busy, peaks, status, oom_mask, bubble};
+        pthread_create(&th[t], NULL, mworker, &jobs[t]);
+    }
+    for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+    return 0;
 }
