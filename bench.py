@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--host-chunk", type=int, default=65536)
     ap.add_argument("--f1-count", type=int, default=65536,
                     help="candidates for the f1 (dual-queue interleaving) measurement; 0 disables it")
+    ap.add_argument("--f3-count", type=int, default=16384,
+                    help="candidates for the f3 (per-layer memory optimisation) measurement; 0 disables it")
     ap.add_argument("--f2-rounds", type=int, default=8, help="MCTS rounds for the f2 measurement; 0 disables it")
     ap.add_argument("--f2-leaves", type=int, default=256)
     ap.add_argument("--f2-rollouts", type=int, default=10)
@@ -308,6 +310,46 @@ def main():
                                 "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
         del d_f1, r_f1
 
+    # ---- per-layer memory optimisation on the first f3-count records
+    f3 = None
+    if args.f3_count > 0:
+        from gen.problem import strategy_menu
+        menu = strategy_menu(pb)
+        model.set_strategies(menu, 10)
+        cnt = min(per, args.f3_count)
+        d_sel = torch.empty(cnt * pb.P * 2 * pb.n_max, dtype=torch.uint8, device=dev)
+        r_f3 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            dip.memopt(model, ws, d_rec, cnt, d_sel, r_f3, None, stream=stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(args.steps, 5))
+        a.record(stream)
+        for _ in range(reps):
+            dip.memopt(model, ws, d_rec, cnt, d_sel, r_f3, None, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tf3 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tf3, op=dist.ReduceOp.MAX)
+        r3 = dip.results_view(r_f3.cpu().numpy())
+        base = dip.results_view(d_res[: cnt * 24].cpu().numpy())
+        ok = (r3["status"] == 0) & (base["status"] == 0)
+        gain = float(np.median(r3["makespan_ns"][ok] / base["makespan_ns"][ok])) if ok.any() else None
+        f3 = {"what": "dip_memopt: per-rank greedy strategy selection under the memory budget (P:569-590) "
+                      "over GPU-built knapsack candidates (P:558-567, S = 10, 3 strategies), then re-timing",
+              "value": cnt * world * reps / (float(tf3[0]) / 1e3), "unit": "candidates/s",
+              "candidates_per_gpu": cnt, "ms_per_call": float(tf3[0]) / reps,
+              "median_makespan_ratio_vs_base": gain}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            import oracle
+            sub = cs.subset(np.arange(min(cnt, 64)))
+            t0 = time.perf_counter()
+            oracle.memopt(pb, sub, menu, S=10, threads=os.cpu_count() or 1)
+            f3["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
+                                "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
+        del d_sel, r_f3
+
     # ---- MCTS segment reordering with batched GPU rollouts, for the
     # split of candidate 0 of this shard (rank 0 only; a search is one planner's job)
     f2 = None
@@ -355,6 +397,7 @@ def main():
                     "frac": bytes_launch / kern_s / 1e9 / hbm_peak,
                     "algorithmic": "record + 24 B result + 4P B peaks per candidate", "peak_source": src},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks, "f1_interleave": f1, "f2_search": f2,
+            "f3_memopt": f3,
             "status_hist": {"ok": hist[0], "oom": hist[1], "deadlock": hist[2], "bad_encoding": hist[3]},
             "winner": {"found": win.found, "global_index": win.global_index, "makespan_ns": win.makespan_ns},
             "setup_s": {"generate": round(t_gen, 1)},

@@ -167,6 +167,38 @@ dip_status dip_timeline(const dip_model *m, dip_workspace *w, const void *d_reco
 dip_status dip_interleave(const dip_model *m, dip_workspace *w, void *d_records, size_t count,
                           dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
 
+/* DIP's per-layer memory optimisation (§5.3).
+ *
+ * dip_set_strategies: the per-layer strategy menu (R-37). f_ns / b_ns /
+ * act_kib are host arrays [n_strat][T], T = sum over modules of (w_max_i + 1), entry (c, tab_off_i + W)
+ * = strategy c's per-layer F ns, B ns and activation KiB of module i at width W (the same column
+ * order as the cost tables of dip_load_cost_model). Strategy 0 must be the tables' own scheme (the
+ * most memory-efficient one); this is the caller's contract. For every stage-pair type
+ * (module, layers per chunk) and width the GPU builds <= S candidates (R-38: fastest,
+ * smallest, fastest of each of S-2 memory buckets; Pareto, memory ascending). 1 <= n_strat <= 8,
+ * 2 <= S <= 16. DIP_ERANGE if a pair total exceeds u32, the enumeration exceeds 2^20 count
+ * vectors per pair, or the menu yields two candidates of equal memory or latency. Replaces a
+ * previous menu. Synchronous. Device model only. */
+dip_status dip_set_strategies(dip_model *m, uint32_t n_strat, const uint32_t *f_ns, const uint32_t *b_ns,
+                              const uint32_t *act_kib, uint32_t S);
+
+/* The candidates of the stage pair (module, layers per chunk, width W) after dip_set_strategies:
+ * out [S][3] host (F ns, B ns, memory KiB), memory ascending; *count receives their number.
+ * DIP_EINVAL if no such pair type exists. */
+dip_status dip_strategy_candidates(const dip_model *m, uint32_t module, uint32_t layers, uint32_t W,
+                                   uint64_t *out, uint32_t *count);
+
+/* Per-rank strategy selection and re-timing of `count` device records (R-39, R-40):
+ * for every (record, rank) the pairs start at candidate 0 and the greedy warm start moves
+ * the pair with the largest latency saving per KiB up while every forward slot it covers stays
+ * within the rank's budget; then the schedules are scored with the selected latencies and
+ * activations (results / peaks / fused argmin key as dip_eval_schedules). d_sel: device
+ * [count][P][2][n_max] u8 out -- sel[c][r][0][p] = candidate of the pair whose forward is the
+ * p-th forward stage, sel[c][r][1][q] = the same for the q-th backward stage (zero beyond n;
+ * unspecified for BAD_ENCODING records). Two launches on `stream`, asynchronous. */
+dip_status dip_memopt(const dip_model *m, dip_workspace *w, const void *d_records, size_t count, uint8_t *d_sel,
+                      dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+
 /* DIP's MCTS segment reordering (§5.1) with batched
  * GPU rollouts. For the given split, classes = (direction, microbatch, module, chunk k) with M > 0
  * (one priority per modality, microbatch and chunk; its M sub-microbatch segments keep a fixed
@@ -185,6 +217,8 @@ typedef struct {
     uint32_t rollouts;        /* random completions per leaf ("e.g., 10 trials") */
     int32_t threads;          /* host threads building rollout records (<= 0: all cores) */
     double alpha, beta;       /* UCB hyper-parameters */
+    int32_t memopt;           /* nonzero: score each rollout after dip_memopt (f3); needs
+                                 dip_set_strategies; the score's LB stays the base-table bound */
 } dip_search_params;
 
 typedef struct {

@@ -67,7 +67,8 @@ def _load():
         lib.oracle_search.restype = ctypes.c_int
         lib.oracle_search.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
                                       ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
-                                      ctypes.c_double, ctypes.c_double] + [ctypes.c_void_p] * 7
+                                      ctypes.c_double, ctypes.c_double] + [ctypes.c_void_p] * 7 + \
+            [ctypes.c_uint32] + [ctypes.c_void_p] * 3 + [ctypes.c_uint32]
         lib.oracle_mem_candidates.restype = ctypes.c_int
         lib.oracle_mem_candidates.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 3 + [ctypes.c_uint32] * 2 + \
             [ctypes.c_void_p]
@@ -158,9 +159,11 @@ def interleave(pb, cands, first: int = 0, count: Optional[int] = None, threads: 
     return bits, res
 
 
-def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float = 1.0, beta: float = 0.5):
-    """S1-S6: MCTS over class orders with batched rounds, scoring rollouts with I1-I6.
-    Returns dict(score, makespan, trace, fwd, bwd, bits, scored)."""
+def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float = 1.0, beta: float = 0.5,
+           menu=None, S: int = 10):
+    """S1-S6: MCTS over class orders with batched rounds, scoring rollouts with I1-I6
+    (then M1-M4 if a strategy menu (f, b, act) is given). Returns dict(score, makespan, trace, fwd,
+    bwd, bits, scored)."""
     from gen import Candidates
     lib = _load()
     dummy = Candidates(pb, 1)
@@ -175,7 +178,7 @@ def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha:
     bits = np.zeros((pb.P, pb.fbw), np.uint32)
     lib.oracle_search(ctypes.byref(bd.pb), pb.n_max, pb.fbw, sp.ctypes.data, seed & ((1 << 64) - 1), rounds, leaves,
                       rollouts, alpha, beta, trace.ctypes.data, ctypes.byref(sc), ctypes.byref(mk), fwd.ctypes.data,
-                      bwd.ctypes.data, bits.ctypes.data, ctypes.byref(scored))
+                      bwd.ctypes.data, bits.ctypes.data, ctypes.byref(scored), *_menu_args(menu, S))
     return dict(score=sc.value, makespan=mk.value, trace=trace, fwd=fwd, bwd=bwd, bits=bits, scored=scored.value)
 
 
@@ -190,6 +193,14 @@ def timeline(pb, cands, x: int):
     if status not in (ST_OK, ST_OOM):
         return status, None, None
     return status, st[:pb.P * 2 * n].reshape(pb.P, 2 * n), en[:pb.P * 2 * n].reshape(pb.P, 2 * n)
+
+
+def _menu_args(menu, S):
+    if menu is None:
+        return (0, None, None, None, S)
+    f, b, a = (np.ascontiguousarray(v, np.uint32) for v in menu)
+    _menu_args.keep = (f, b, a)
+    return (f.shape[0], f.ctypes.data, b.ctypes.data, a.ctypes.data, S)
 
 
 def mem_candidates(f, b, act, layers: int, S: int):

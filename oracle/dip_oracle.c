@@ -635,8 +635,10 @@ int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint
  *   S2 a sequence (permutation of the Cn classes) gives priority Cn-1-p to the class at position p
  *      (P:481); the forward / backward queue order of a rank = repeatedly the ready segment of the
  *      highest priority (within a class: j ascending).
- *   S3 rollout score: interleave (I1-I6) and score LB / makespan if OK, else 0, with LB the
- *      busiest rank's summed latency of the split.
+ *   S3 rollout score: interleave (I1-I6) -- and, if a strategy menu is given, the per-layer
+ *      memory optimisation (M1-M4, "undergoes pipeline stage interleaving ... and per-layer
+ *      memory optimization") -- and score LB / makespan if OK, else 0, with LB the busiest rank's
+ *      summed latency of the split (base tables).
  *   S4 selection: from the root, while the node has all its children, move to the child of
  *      largest s^alpha + beta * sqrt(ln N_x / N_v) (ties: first child, i.e. lowest class); counts
  *      include the virtual visits of the current round.
@@ -656,6 +658,14 @@ static uint64_t smix(uint64_t x) {
 }
 
 typedef struct { int parent, cls, depth, nch, cap; int *ch; double s; uint32_t N, vl; } snode;
+
+/* M1-M4 (below): per-layer memory optimisation of one schedule, used by S3 when a menu is given */
+typedef struct {
+    uint32_t n_strat, S;
+    const uint32_t *f, *b, *act;    /* [n_strat][tab_off[nmod]] per-layer menu (M1) */
+} omenu;
+static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, uint64_t x, uint8_t *sel,
+                       ores *res, uint64_t *peaks);
 
 /* S2: queue order of one direction from class priorities (plain selection, O(n^2)) */
 static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *base, const int *clsof, uint32_t C,
@@ -723,7 +733,9 @@ static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *ba
 int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_t *split, uint64_t seed,
                   uint32_t rounds, uint32_t leaves, uint32_t rollouts, double alpha, double beta,
                   double *trace, double *best_score, uint64_t *best_makespan, uint16_t *best_fwd,
-                  uint16_t *best_bwd, uint32_t *best_bits, uint64_t *scored_out) {
+                  uint16_t *best_bwd, uint32_t *best_bits, uint64_t *scored_out,
+                  uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma, uint32_t S) {
+    omenu mn = {n_strat, S, mf, mb, ma};   /* n_strat = 0: rollouts are interleaved only */
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
     uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
     int *clsof = malloc(sizeof(int) * m * nm);
@@ -837,6 +849,13 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
         for (uint32_t x = 0; x < cnt; x++) {
             ores r;
             interleave_one(pb, &cs, x, bits + (size_t)x * P * fbw, &r, NULL);
+            if (n_strat) {                                  /* then per-layer memory opt. (M1-M4) */
+                ocands c1 = {n_max, fbw, spl + (size_t)x * m * nm, nn_ + x, fw + (size_t)x * n_max,
+                             bw + (size_t)x * n_max, bits + (size_t)x * P * fbw};
+                uint8_t *sel = malloc((size_t)P * 2 * n_max);
+                memopt_one(pb, &mn, &c1, 0, sel, &r, NULL);
+                free(sel);
+            }
             double sc = r.status == ST_OK ? LB / (double)r.makespan : 0.0;
             if (sc > lb[owner[x]]) lb[owner[x]] = sc;
             if (sc > best) {
@@ -984,11 +1003,6 @@ int oracle_mem_candidates(uint32_t n_strat, const uint32_t *f, const uint32_t *b
     free(all); free(pick);
     return (int)k;
 }
-
-typedef struct {
-    uint32_t n_strat, S;
-    const uint32_t *f, *b, *act;    /* [n_strat][tab_off[nmod]] per-layer menu (M1) */
-} omenu;
 
 /* M2-M4 for candidate x: sel [P][2][n_max] (candidate index of the pair at forward position p /
  * backward position q), then the re-timed result. */

@@ -293,6 +293,8 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
 dip_status dip_model_free(dip_model *m) {
     if (!m) return DIP_OK;
     if (m->d_blob) cudaFree(m->d_blob);
+    if (m->d_ctab) cudaFree(m->d_ctab);
+    if (m->d_crow) cudaFree(m->d_crow);
     delete m;
     return DIP_OK;
 }
@@ -409,10 +411,11 @@ dip_status dip_workspace_free(dip_workspace *w) {
 extern "C++" {
 dip_status diph::launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                                uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
-                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out) {
+                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out, const uint8_t *sel) {
     KParams kp = M->kp;
     kp.records = static_cast<const uint8_t *>(d_records);
     kp.records_out = records_out;
+    kp.sel = sel;
     kp.tl_start = nullptr;
     kp.tl_end = nullptr;
     kp.count = count;
@@ -484,6 +487,7 @@ dip_status dip_timeline(const dip_model *M, dip_workspace *w, const void *d_reco
     KParams kp = M->kp;
     kp.records = static_cast<const uint8_t *>(d_records);
     kp.records_out = nullptr;
+    kp.sel = nullptr;
     kp.tl_start = d_start;
     kp.tl_end = d_end;
     kp.count = count;

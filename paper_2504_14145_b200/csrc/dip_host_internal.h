@@ -56,6 +56,14 @@ struct dip_model {
     int G = 32, cpg = 1, wpb = 1, bps = 1, grid = 1, num_sms = 148;
     size_t smem = 0;
     uint64_t mk_bound = 0;
+    // f3 (per-layer memory optimisation): strategy menu -> candidate table
+    uint32_t n_strat = 0, S = 0;
+    std::vector<uint32_t> t_mod, t_lay, t_base;   // candidate types (module, layers per chunk)
+    std::vector<uint4> h_ctab;                    // host copy of the candidate table
+    uint4 *d_ctab = nullptr;
+    int32_t *d_crow = nullptr;
+    uint32_t mo_warp_bytes = 0;
+    int mo_grid = 0;
 };
 
 struct dip_workspace {
@@ -85,6 +93,7 @@ struct dip_comm {
 namespace diph {
 dip_status launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                         uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
-                        uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out = nullptr);
+                        uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out = nullptr,
+                        const uint8_t *sel = nullptr);
 bool fused_ok(const dip_model *M, uint32_t idx_bits);
 }  // namespace diph

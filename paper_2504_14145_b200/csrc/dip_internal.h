@@ -39,6 +39,10 @@ struct KParams {
     const uint8_t *records;
     uint8_t *records_out;       // non-null: interleave mode (f1) writes the F/B bit rows here
     uint64_t *tl_start, *tl_end;  // non-null: timeline mode, [count][P][2*n_max] per-slot start / end
+    const uint8_t *sel;         // non-null: f3 mode, [count][P][2][n_max] selected candidate per stage pair
+    const uint4 *ctab;          // f3 candidates {F ns, B ns, act KiB, count} per (type, W, c)
+    const int32_t *crow;        // f3: per chunk row, ctab base of its (module, layers) type - tab_off * S
+    uint32_t S;                 // f3: candidates per (type, W)
     uint64_t count, index_base;
     dip_result *results;
     uint32_t *peaks;
@@ -48,7 +52,19 @@ struct KParams {
     uint32_t fused_key, idx_bits;
 };
 
+// f3 candidate generation: one thread per (type, W); a type = (module i, layers per chunk l)
+struct MCandParams {
+    uint32_t n_items, n_types, n_strat, S, T;
+    const uint32_t *t_item, *t_lay, *t_toff, *t_base;   // [n_types]: first item, l, tab_off[i], ctab base
+    const uint32_t *mf, *mb, *ma;                       // menu [n_strat][T]
+    uint4 *ctab;                                        // out: [sum (w_max_i + 1)] x S
+};
+
 cudaError_t launch_eval(const KParams &kp, int G, int grid, int block, size_t smem, cudaStream_t s);
+cudaError_t launch_mcand(const MCandParams &p, cudaStream_t s);
+cudaError_t prepare_memopt(size_t smem);
+cudaError_t occupancy_memopt(size_t smem, int *blocks_per_sm);
+cudaError_t launch_memopt(const KParams &kp, uint8_t *sel, uint32_t warp_bytes, int grid, cudaStream_t s);
 cudaError_t prepare_eval(int G, size_t smem);
 cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm);
 cudaError_t launch_scan_argmin(const dip_result *res, uint64_t count, uint64_t index_base,

@@ -110,7 +110,9 @@ __device__ __noinline__ void spill_keep(unsigned long long *spill, uint32_t d, u
     spill[(d ? (P + r) : r) * n_max + idx - RING_D] = v;
 }
 
-template <int G, int MODE>   // MODE 0: score the given schedules; MODE 1: build them (f1) and score
+// MODE 0: score the given schedules; MODE 1: build them (f1) and score; MODE 2: score and record
+// every stage's start / end (f4); MODE 3: score with each stage pair's selected memory strategy (f3)
+template <int G, int MODE>
 __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t blob_bar;
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         uint64_t tlast = 0, busy = 0;
         uint32_t cur = 0, peak = 0;
         const uint32_t S2 = 2 * n;
-        if (MODE != 1) {   // MODE 0: score; MODE 2: score and record every stage's start/end
+        if (MODE != 1) {   // MODE 0 / 3: score; MODE 2: score and record every stage's start/end
         // ---------------- K3: lock-step wavefront longest path ----------------
         // Per round every lane of the group tries its next slot (F if bit t is 0, else B):
         // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
@@ -378,8 +380,14 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
             __syncwarp();
             if (ready) {
-                const uint64_t lat = (uint64_t)lay * (d ? T.y : T.x);
-                const uint32_t act = lay * T.z;
+                uint64_t lat = (uint64_t)lay * (d ? T.y : T.x);
+                uint32_t act = lay * T.z;
+                if (MODE == 3) {   // f3: the stage pair's selected memory-strategy candidate
+                    const uint32_t c = kp.sel[((cand * P + r) * 2 + d) * (uint64_t)n_max + idx];
+                    const uint4 E = __ldg(&kp.ctab[__ldg(&kp.crow[((e.x >> 12) & 0xFFFu) + r]) + (int32_t)((e.x & 0xFFFu) * kp.S + c)]);
+                    lat = d ? E.y : E.x;
+                    act = E.z;
+                }
                 const uint64_t st = dep > tlast ? dep : tlast;
                 const uint64_t end = st + lat;
                 tlast = end;
@@ -428,8 +436,13 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             while (t < S2) {
                 if ((t & 31) == 0 && t > 0) wcur = ldg32(rec + kp.off_fb + 4 * ((t >> 5) * P + r));
                 const bool b1 = (wcur >> (t & 31)) & 1u;
-                const uint2 ee = posAll[(b1 ? n_max + bi++ : fi++)];
-                const uint32_t a = (uint32_t)layers[((ee.x >> 12) & 0xFFFu) + r] * tab[ee.x & 0xFFFu].z;
+                const uint32_t pi = b1 ? bi++ : fi++;
+                const uint2 ee = posAll[(b1 ? n_max : 0) + pi];
+                uint32_t a = (uint32_t)layers[((ee.x >> 12) & 0xFFFu) + r] * tab[ee.x & 0xFFFu].z;
+                if (MODE == 3) {
+                    const uint32_t c = kp.sel[((cand * P + r) * 2 + (b1 ? 1 : 0)) * (uint64_t)n_max + pi];
+                    a = __ldg(&kp.ctab[__ldg(&kp.crow[((ee.x >> 12) & 0xFFFu) + r]) + (int32_t)((ee.x & 0xFFFu) * kp.S + c)]).z;
+                }
                 if (!b1) { cur += a; peak = cur > peak ? cur : peak; }
                 else cur -= a;
                 t++;
@@ -632,6 +645,7 @@ template <int G>
 static cudaError_t launch_g(const KParams &kp, int grid, int block, size_t smem, cudaStream_t s) {
     if (kp.records_out) dip_eval_kernel<G, 1><<<grid, block, smem, s>>>(kp);
     else if (kp.tl_start) dip_eval_kernel<G, 2><<<grid, block, smem, s>>>(kp);
+    else if (kp.sel) dip_eval_kernel<G, 3><<<grid, block, smem, s>>>(kp);
     else dip_eval_kernel<G, 0><<<grid, block, smem, s>>>(kp);
     return cudaGetLastError();
 }
@@ -653,21 +667,25 @@ static const void *kernel_for(int G, int mode) {
     case 16: return kfun<4, 0>();
     case 17: return kfun<4, 1>();
     case 18: return kfun<4, 2>();
+    case 19: return kfun<4, 3>();
     case 32: return kfun<8, 0>();
     case 33: return kfun<8, 1>();
     case 34: return kfun<8, 2>();
+    case 35: return kfun<8, 3>();
     case 64: return kfun<16, 0>();
     case 65: return kfun<16, 1>();
     case 66: return kfun<16, 2>();
+    case 67: return kfun<16, 3>();
     case 128: return kfun<32, 0>();
     case 129: return kfun<32, 1>();
     case 130: return kfun<32, 2>();
+    case 131: return kfun<32, 3>();
     default: return nullptr;
     }
 }
 
 cudaError_t prepare_eval(int G, size_t smem) {
-    for (int mode = 0; mode < 3; mode++) {
+    for (int mode = 0; mode < 4; mode++) {
         const void *f = kernel_for(G, mode);
         if (!f) return cudaErrorInvalidValue;
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -678,7 +696,7 @@ cudaError_t prepare_eval(int G, size_t smem) {
 
 cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm) {
     int best = 1 << 30;
-    for (int mode = 0; mode < 2; mode++) {
+    for (int mode = 0; mode < 2; mode++) {   // the scorer and f1 set the shape; modes 2, 3 reuse it
         const void *f = kernel_for(G, mode);
         if (!f) return cudaErrorInvalidValue;
         int b = 0;

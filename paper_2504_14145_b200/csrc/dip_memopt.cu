@@ -1,0 +1,372 @@
+// dip_memopt.cu -- SURVEY §8(f) row f3: DIP's per-layer memory optimisation (§5.3,
+// P:550-590) on sm_100a. Two kernels:
+//
+//  * dip_mcand_kernel (readings R-37/R-38): the <= S strategy candidates of every stage
+//    pair type (module i, layers per chunk l, width W) -- one thread per (type, W) enumerates the
+//    strategy-count vectors of the l identical layers (the exact multiple-choice knapsack), keeps
+//    the fastest, the most memory-efficient and the fastest of each of the S-2 memory buckets,
+//    drops duplicates / dominated entries and sorts by memory. Runs once per menu.
+//  * dip_memopt_kernel (R-39): the per-rank selection for a batch of schedules -- one
+//    warp per (schedule, rank). The warp rebuilds the rank's order from the record (forward
+//    position p -> its point range [p, e_p) over the rank's forward slots, e_p = slot of the
+//    pair's backward - its backward position), builds the slack profile of candidate 0 with a
+//    difference array + warp scan, then runs the greedy: every lane proposes its best pair
+//    (largest latency saving per KiB, exact u64 cross-multiplication, ties to the lower p), a
+//    5-step shuffle reduction picks the winner, the lanes subtract its memory step over its range
+//    and refresh the cached range-minimum slack of the pairs that overlap it. A pair whose step no
+//    longer fits is dead for good (slack only decreases). Output: sel[x][r][0][p] / [1][q].
+//  The re-timing with the selected candidates (M4) is the scorer's MODE 3 (dip_kernels.cu).
+#include <cstdint>
+
+#include "dip_internal.h"
+
+namespace dipk {
+
+namespace {
+
+__device__ __forceinline__ uint32_t ldg32u(const uint8_t *p) { return __ldg(reinterpret_cast<const uint32_t *>(p)); }
+
+struct MC { unsigned long long f, b, mem; };
+
+__device__ __forceinline__ bool mc_before(const MC &a, const MC &b, bool by_mem) {
+    const unsigned long long la = a.f + a.b, lb = b.f + b.b;
+    if (by_mem) {
+        if (a.mem != b.mem) return a.mem < b.mem;
+        if (la != lb) return la < lb;
+    } else {
+        if (la != lb) return la < lb;
+        if (a.mem != b.mem) return a.mem < b.mem;
+    }
+    return a.f < b.f;
+}
+
+}  // namespace
+
+constexpr int MAX_S = 16;
+constexpr int MAX_STRAT = 8;
+
+__global__ void __launch_bounds__(128) dip_mcand_kernel(const MCandParams p) {
+    const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= p.n_items) return;
+    uint32_t t = 0;
+    while (t + 1 < p.n_types && p.t_item[t + 1] <= item) t++;
+    const uint32_t W = item - p.t_item[t], L = p.t_lay[t], C = p.n_strat, S = p.S;
+    const uint32_t col = p.t_toff[t] + W;
+    uint4 *out = p.ctab + p.t_base[t] + (size_t)W * S;
+    if (L == 0) {   // a chunk without layers: one empty candidate
+        out[0] = make_uint4(0u, 0u, 0u, 1u);
+        for (uint32_t c = 1; c < S; c++) out[c] = make_uint4(0u, 0u, 0u, 1u);
+        return;
+    }
+    uint32_t fv[MAX_STRAT], bv[MAX_STRAT], av[MAX_STRAT];
+    for (uint32_t c = 0; c < C; c++) {
+        fv[c] = __ldg(&p.mf[(size_t)c * p.T + col]);
+        bv[c] = __ldg(&p.mb[(size_t)c * p.T + col]);
+        av[c] = __ldg(&p.ma[(size_t)c * p.T + col]);
+    }
+    // every count vector (n_0 .. n_{C-1}), sum L, in odometer order over the first C-1 counts
+    MC fast{0, 0, 0}, small{0, 0, 0}, bb[MAX_S];
+    bool have[MAX_S];
+    for (int u = 0; u < MAX_S; u++) have[u] = false;
+    for (int pass = 0; pass < 2; pass++) {
+        unsigned long long span = 0;
+        if (pass == 1) {
+            if (!(S > 2 && fast.mem > small.mem)) break;
+            span = fast.mem - small.mem;
+        }
+        uint32_t cnt[MAX_STRAT];
+        for (uint32_t c = 0; c < C; c++) cnt[c] = 0;
+        bool first = true;
+        for (;;) {
+            uint32_t used = 0;
+            for (uint32_t c = 0; c + 1 < C; c++) used += cnt[c];
+            if (used <= L) {
+                cnt[C - 1] = L - used;
+                MC x{0, 0, 0};
+                for (uint32_t c = 0; c < C; c++) {
+                    x.f += (unsigned long long)cnt[c] * fv[c];
+                    x.b += (unsigned long long)cnt[c] * bv[c];
+                    x.mem += (unsigned long long)cnt[c] * av[c];
+                }
+                if (pass == 0) {
+                    if (first) { fast = x; small = x; first = false; }
+                    else {
+                        if (mc_before(x, fast, false)) fast = x;
+                        if (mc_before(x, small, true)) small = x;
+                    }
+                } else if (x.mem < fast.mem) {
+                    // bucket u: [small + floor(span u / (S-2)), small + floor(span (u+1) / (S-2)))
+                    const unsigned long long d = x.mem - small.mem;
+                    const uint32_t u = (uint32_t)(((d + 1) * (S - 2) - 1) / span);
+                    if (!have[u] || mc_before(x, bb[u], false)) { bb[u] = x; have[u] = true; }
+                }
+            }
+            uint32_t c = 0;
+            while (c + 1 < C) {
+                if (++cnt[c] <= L) break;
+                cnt[c] = 0;
+                c++;
+            }
+            if (c + 1 >= C) break;
+        }
+    }
+    MC pick[MAX_S + 2];
+    uint32_t np = 0;
+    pick[np++] = fast;
+    pick[np++] = small;
+    if (S > 2 && fast.mem > small.mem)
+        for (uint32_t u = 0; u < S - 2; u++)
+            if (have[u]) pick[np++] = bb[u];
+    uint32_t k = 0;
+    for (uint32_t x = 0; x < np; x++) {
+        bool drop = false;
+        for (uint32_t y = 0; y < np && !drop; y++) {
+            if (y == x) continue;
+            const unsigned long long lx = pick[x].f + pick[x].b, ly = pick[y].f + pick[y].b;
+            const bool same = pick[y].f == pick[x].f && pick[y].b == pick[x].b && pick[y].mem == pick[x].mem;
+            if (same && y < x) drop = true;
+            if (!same && pick[y].mem <= pick[x].mem && ly <= lx && (pick[y].mem < pick[x].mem || ly < lx)) drop = true;
+        }
+        if (!drop) pick[k++] = pick[x];
+    }
+    for (uint32_t x = 1; x < k; x++)
+        for (uint32_t y = x; y > 0 && pick[y].mem < pick[y - 1].mem; y--) {
+            const MC tmp = pick[y];
+            pick[y] = pick[y - 1];
+            pick[y - 1] = tmp;
+        }
+    for (uint32_t c = 0; c < S; c++) {
+        const MC &v = pick[c < k ? c : 0];
+        out[c] = c < k ? make_uint4((uint32_t)v.f, (uint32_t)v.b, (uint32_t)v.mem, k) : make_uint4(0u, 0u, 0u, k);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// per (schedule, rank) selection: one warp each, persistent over an atomic work counter
+__global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8_t *sel_out, uint32_t warp_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const unsigned FULL = 0xffffffffu;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t P = kp.P, nmod = kp.nmod, nq = kp.m * kp.nmod, n_max = kp.n_max, S = kp.S;
+    const ModInfo *mi = reinterpret_cast<const ModInfo *>(kp.blob + kp.b_modinfo);
+    const uint32_t *segdec = reinterpret_cast<const uint32_t *>(kp.blob + kp.b_segdec);
+    const uint32_t *woff = reinterpret_cast<const uint32_t *>(kp.blob + kp.b_woff);
+    const uint16_t *wtab = reinterpret_cast<const uint16_t *>(kp.blob + kp.b_wtab);
+    const uint16_t *nbi = reinterpret_cast<const uint16_t *>(kp.blob + kp.b_nbi);
+    const uint32_t *budget = reinterpret_cast<const uint32_t *>(kp.blob + kp.b_budget);
+
+    uint8_t *wa = smem + (size_t)warp * warp_bytes;
+    long long *slack = reinterpret_cast<long long *>(wa);                  // [n_max]
+    long long *ms = slack + n_max;                                          // [n_max] cached range-min slack
+    int32_t *cb = reinterpret_cast<int32_t *>(ms + n_max);                  // [n_max] ctab row of pair p
+    uint16_t *fw = reinterpret_cast<uint16_t *>(cb + n_max);                // [n_max] forward sequence
+    uint16_t *invB = fw + n_max;                                            // segment -> backward position
+    uint16_t *bsl = invB + n_max;                                           // slot of the q-th backward
+    uint16_t *eP = bsl + n_max;                                             // end of pair p's point range
+    uint8_t *cur = reinterpret_cast<uint8_t *>(eP + n_max);                 // selected candidate
+    uint8_t *ncand = cur + n_max;
+    uint8_t *dead = ncand + n_max;
+    uint8_t *Mb = dead + n_max;                                             // [nq]
+
+    const long long INF = 0x7FFFFFFFFFFFFFFFll;
+    for (;;) {
+        unsigned long long item = 0;
+        if (lane == 0) item = atomicAdd(kp.counter, 1ull);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= kp.count * P) break;
+        const uint64_t x = item / P;
+        const uint32_t r = (uint32_t)(item - x * P);
+        const uint8_t *rec = kp.records + x * (uint64_t)kp.stride;
+        uint8_t *selF = sel_out + (x * P + r) * 2ull * n_max, *selB = selF + n_max;
+
+        // ---- decode (necessary conditions of a valid record; the scorer makes the verdict)
+        const uint32_t hdr = ldg32u(rec);
+        const uint32_t n = hdr & 0xFFFFu;
+        bool bad = (hdr >> 16) != 0 || n > n_max;
+        uint32_t nsum = 0;
+        for (uint32_t q = lane; q < nq && !bad; q += 32) {
+            const uint32_t b = q / nmod, i = q - b * nmod;
+            const uint32_t N = __ldg(&nbi[q]), Mx = __ldg(&mi[i].max_split);
+            uint32_t M;
+            if (Mx > 1) {
+                const uint32_t nib = b * kp.nsplit + __ldg(&mi[i].nib_slot);
+                M = (__ldg(rec + kp.off_nib + (nib >> 1)) >> ((nib & 1) * 4)) & 15u;
+            } else {
+                M = N > 0 ? 1u : 0u;
+            }
+            if ((N == 0) != (M == 0) || M > (N < Mx ? N : Mx)) bad = true;
+            Mb[q] = (uint8_t)M;
+            nsum += M * __ldg(&mi[i].K);
+        }
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(FULL, nsum, o);
+        if (nsum != n) bad = true;
+        bad = __any_sync(FULL, bad);
+        if (!bad) {
+            for (uint32_t p = lane; p < n_max; p += 32) {
+                fw[p] = __ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_fwd) + p);
+                invB[p] = 0xFFFFu;
+            }
+            __syncwarp();
+            for (uint32_t q = lane; q < n; q += 32) {
+                const uint32_t s = __ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_bwd) + q);
+                if (s >= n_max) bad = true;
+                else invB[s] = (uint16_t)q;
+            }
+            // the rank's bit row: slot of every backward stage (prefix popcounts across lanes)
+            uint32_t carry = 0;
+            for (uint32_t w0 = 0; w0 < kp.fbw; w0 += 32) {
+                const uint32_t w = w0 + lane;
+                uint32_t word = 0;
+                if (w < kp.fbw) {
+                    word = ldg32u(rec + kp.off_fb + 4 * (w * P + r));
+                    const uint32_t lim = 2 * n;
+                    if (32 * w >= lim) word = 0;
+                    else if (32 * w + 32 > lim) word &= (1u << (lim - 32 * w)) - 1u;
+                }
+                const uint32_t pc = __popc(word);
+                uint32_t incl = pc;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                uint32_t q = carry + incl - pc;
+                while (word) {
+                    const uint32_t bit = __ffs(word) - 1;
+                    word &= word - 1;
+                    if (q < n_max) bsl[q] = (uint16_t)(32 * w + bit);
+                    q++;
+                }
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+            if (carry != n) bad = true;
+            bad = __any_sync(FULL, bad);
+            __syncwarp();
+        }
+        if (!bad) {   // pairs: range, candidate row, candidate 0's memory in the difference array
+            for (uint32_t k = lane; k < n; k += 32) slack[k] = 0;
+            __syncwarp();
+            for (uint32_t p = lane; p < n; p += 32) {
+                const uint32_t s = fw[p];
+                const uint32_t q = s < n_max ? invB[s] : 0xFFFFu;
+                if (q == 0xFFFFu) { bad = true; continue; }
+                const uint32_t e = (uint32_t)bsl[q] - q;
+                eP[p] = (uint16_t)e;
+                const uint32_t dc = __ldg(&segdec[s]);
+                const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
+                const uint32_t qq = b * nmod + i, M = Mb[qq];
+                const uint32_t W = __ldg(&wtab[__ldg(&woff[qq]) + M * (M - 1) / 2 + j]);
+                const int32_t row = __ldg(&kp.crow[__ldg(&mi[i].lay_off) + k * P + r]) + (int32_t)((__ldg(&mi[i].tab_off) + W) * S);
+                cb[p] = row;
+                const uint4 E = __ldg(&kp.ctab[row]);
+                ncand[p] = (uint8_t)E.w;
+                cur[p] = 0;
+                dead[p] = 0;
+                if (e > p) {
+                    atomicAdd(reinterpret_cast<unsigned long long *>(&slack[p]), (unsigned long long)E.z);
+                    if (e < n) atomicAdd(reinterpret_cast<unsigned long long *>(&slack[e]), (unsigned long long)(-(long long)E.z));
+                }
+            }
+            bad = __any_sync(FULL, bad);
+            __syncwarp();
+        }
+        if (bad) {
+            for (uint32_t p = lane; p < 2 * n_max; p += 32) selF[p] = 0;
+            continue;
+        }
+        // prefix sum -> slack = budget - used at every forward slot
+        const long long bud = (long long)__ldg(&budget[r]);
+        bool feasible = true;
+        {
+            long long run = 0;
+            for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                long long v = k < n ? slack[k] : 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long u = __shfl_up_sync(FULL, v, o);
+                    if (lane >= o) v += u;
+                }
+                if (k < n) {
+                    slack[k] = bud - (run + v);
+                    if (slack[k] < 0) feasible = false;
+                }
+                run += __shfl_sync(FULL, v, 31);
+            }
+            feasible = __all_sync(FULL, feasible);
+            __syncwarp();
+        }
+        if (feasible) {
+            for (uint32_t p = lane; p < n; p += 32) {
+                long long mn = INF;
+                for (uint32_t k = p; k < eP[p]; k++) mn = slack[k] < mn ? slack[k] : mn;
+                ms[p] = mn;
+            }
+            __syncwarp();
+            for (;;) {
+                // each lane's best upgrade: max dl/dm, ties to the lower p
+                uint32_t bdl = 0, bdm = 1, bp = 0xFFFFFFFFu;
+                for (uint32_t p = lane; p < n; p += 32) {
+                    if (dead[p] || cur[p] + 1u >= ncand[p]) continue;
+                    const uint4 E0 = __ldg(&kp.ctab[cb[p] + cur[p]]), E1 = __ldg(&kp.ctab[cb[p] + cur[p] + 1]);
+                    const uint32_t dm = E1.z - E0.z, dl = (E0.x + E0.y) - (E1.x + E1.y);
+                    if ((long long)dm > ms[p]) { dead[p] = 1; continue; }
+                    if (bp == 0xFFFFFFFFu || (unsigned long long)dl * bdm > (unsigned long long)bdl * dm) { bdl = dl; bdm = dm; bp = p; }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const uint32_t ol = __shfl_xor_sync(FULL, bdl, o), om = __shfl_xor_sync(FULL, bdm, o),
+                                   op = __shfl_xor_sync(FULL, bp, o);
+                    bool take;
+                    if (op == 0xFFFFFFFFu) take = false;
+                    else if (bp == 0xFFFFFFFFu) take = true;
+                    else {
+                        const unsigned long long a = (unsigned long long)ol * bdm, c = (unsigned long long)bdl * om;
+                        take = a > c || (a == c && op < bp);
+                    }
+                    if (take) { bdl = ol; bdm = om; bp = op; }
+                }
+                if (bp == 0xFFFFFFFFu) break;
+                const uint32_t a0 = bp, a1 = eP[bp];
+                __syncwarp();
+                if (lane == 0) cur[a0] = (uint8_t)(cur[a0] + 1);
+                for (uint32_t k = a0 + lane; k < a1; k += 32) slack[k] -= (long long)bdm;
+                __syncwarp();
+                for (uint32_t p = lane; p < n; p += 32) {   // refresh the range minimum where it overlaps
+                    const uint32_t lo = p > a0 ? p : a0, hi = eP[p] < a1 ? eP[p] : a1;
+                    if (lo >= hi) continue;
+                    long long mn = ms[p];
+                    for (uint32_t k = lo; k < hi; k++) mn = slack[k] < mn ? slack[k] : mn;
+                    ms[p] = mn;
+                }
+                __syncwarp();
+            }
+        }
+        for (uint32_t p = lane; p < n_max; p += 32) {
+            const uint8_t c = p < n ? cur[p] : 0;
+            selF[p] = c;
+            if (p < n) selB[invB[fw[p]]] = c;
+        }
+        if (n < n_max)
+            for (uint32_t q = n + lane; q < n_max; q += 32) selB[q] = 0;
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_mcand(const MCandParams &p, cudaStream_t s) {
+    const uint32_t blocks = (p.n_items + 127) / 128;
+    dip_mcand_kernel<<<blocks ? blocks : 1, 128, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t prepare_memopt(size_t smem) {
+    return cudaFuncSetAttribute(dip_memopt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t occupancy_memopt(size_t smem, int *blocks_per_sm) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dip_memopt_kernel, 128, smem);
+}
+
+cudaError_t launch_memopt(const KParams &kp, uint8_t *sel, uint32_t warp_bytes, int grid, cudaStream_t s) {
+    dip_memopt_kernel<<<grid, 128, 4 * (size_t)warp_bytes, s>>>(kp, sel, warp_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace dipk

@@ -12,7 +12,8 @@
 // class; expansion: the next child in class order; rollouts: uniformly random
 // completions of the remaining positions (counter-based splitmix64 stream per rollout); score
 // (P:499): LB / makespan for a feasible (OK) schedule, 0 otherwise, LB = the busiest rank's total
-// latency; backpropagation: s_v = max(s_v, best trial), N_v += 1 along the path.
+// latency (base tables); with memopt the rollout is interleaved and then memory-optimised (f3,
+// P:498 "undergoes pipeline stage interleaving ... and per-layer memory optimization"); backpropagation: s_v = max(s_v, best trial), N_v += 1 along the path.
 // Batching (the GPU analogue of the paper's parallel workers sharing one tree): each
 // round selects `leaves` leaves with a virtual visit on every node of each selected path, expands
 // them, scores all their rollouts in one dip_interleave launch, then backpropagates leaf by leaf.
@@ -141,6 +142,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
                                  dip_search_result *out, void *stream) {
     if (!Md || !w || w->model != Md || !split || !prm || !out) return fail(DIP_EINVAL, "null argument");
     if (prm->rounds == 0 || prm->leaves == 0 || prm->rollouts == 0) return fail(DIP_EINVAL, "empty budget");
+    if (prm->memopt && !Md->S) return fail(DIP_EINVAL, "memopt rollouts need a strategy menu (dip_set_strategies)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Setup S;
     S.P = Md->P; S.nm = Md->nmod; S.m = Md->m;
@@ -185,8 +187,13 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     std::vector<dip_result> h_res(cap);
     uint8_t *d_rec = nullptr;
     dip_result *d_res = nullptr;
+    uint8_t *d_sel = nullptr;
     CUDA_TRY(cudaMalloc(&d_rec, cap * Md->stride));
     if (cudaMalloc(&d_res, cap * sizeof(dip_result)) != cudaSuccess) { cudaFree(d_rec); return fail(DIP_ENOMEM, "search buffers"); }
+    if (prm->memopt && cudaMalloc(&d_sel, cap * Md->P * 2ull * Md->n_max) != cudaSuccess) {
+        cudaFree(d_rec); cudaFree(d_res);
+        return fail(DIP_ENOMEM, "search buffers");
+    }
     std::vector<Node> tree(1);
     tree.reserve(1 + (size_t)prm->rounds * B);
     double best = -1.0;
@@ -280,6 +287,10 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
         }
         status = dip_interleave(Md, w, d_rec, cnt, d_res, nullptr, stream);
         if (status != DIP_OK) break;
+        if (prm->memopt) {   // interleaving, then per-layer memory optimisation (f3)
+            status = dip_memopt(Md, w, d_rec, cnt, d_sel, d_res, nullptr, stream);
+            if (status != DIP_OK) break;
+        }
         if (cudaMemcpyAsync(h_res.data(), d_res, cnt * sizeof(dip_result), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess) {
             status = fail(DIP_ECUDA, "search D2H");
@@ -310,6 +321,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     }
     cudaFree(d_rec);
     cudaFree(d_res);
+    if (d_sel) cudaFree(d_sel);
     if (status != DIP_OK) return status;
     out->found = best > 0.0;
     out->makespan_ns = out->found ? best_mk : ~0ull;

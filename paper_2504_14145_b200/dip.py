@@ -53,7 +53,7 @@ class _CandBatch(ctypes.Structure):
 class _SearchParams(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("rounds", ctypes.c_uint32), ("leaves", ctypes.c_uint32),
                 ("rollouts", ctypes.c_uint32), ("threads", ctypes.c_int32), ("alpha", ctypes.c_double),
-                ("beta", ctypes.c_double)]
+                ("beta", ctypes.c_double), ("memopt", ctypes.c_int32)]
 
 
 class _SearchResult(ctypes.Structure):
@@ -114,6 +114,10 @@ def lib():
     L.dip_timeline.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
     L.dip_compile_plan.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(ctypes.c_uint32)]
     L.dip_validate_plan.argtypes = [vp, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_int32)]
+    L.dip_set_strategies.argtypes = [vp, ctypes.c_uint32, vp, vp, vp, ctypes.c_uint32]
+    L.dip_strategy_candidates.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp,
+                                          ctypes.POINTER(ctypes.c_uint32)]
+    L.dip_memopt.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
     L.dip_comm_unique_id.argtypes = [vp]
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
@@ -122,7 +126,8 @@ def lib():
               "dip_argmin",
               "dip_eval_host",
               "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key",
-              "dip_timeline", "dip_compile_plan", "dip_validate_plan"):
+              "dip_timeline", "dip_compile_plan", "dip_validate_plan",
+              "dip_set_strategies", "dip_strategy_candidates", "dip_memopt"):
         getattr(L, f).restype = st
     L.dip_launch_count.restype = ctypes.c_uint64
     L.dip_launch_count.argtypes = []
@@ -220,6 +225,23 @@ class Model:
                "dip_encode_candidates")
         return out
 
+    def set_strategies(self, menu, S: int = 10):
+        """f3: per-layer strategy menu (f, b, act) arrays [n_strat, T] -> the GPU
+        candidate table of every stage-pair type."""
+        f, b, a = (np.ascontiguousarray(v, np.uint32) for v in menu)
+        assert f.shape == b.shape == a.shape and f.ndim == 2
+        _check(lib().dip_set_strategies(self.handle, f.shape[0], f.ctypes.data, b.ctypes.data, a.ctypes.data, S),
+               "dip_set_strategies")
+        self.S = S
+
+    def strategy_candidates(self, module: int, layers: int, W: int):
+        """the (F ns, B ns, mem KiB) candidates of one stage-pair type at width W"""
+        out = np.zeros((16, 3), np.uint64)
+        k = ctypes.c_uint32()
+        _check(lib().dip_strategy_candidates(self.handle, module, layers, W, out.ctypes.data, ctypes.byref(k)),
+               "dip_strategy_candidates")
+        return [tuple(int(v) for v in out[x]) for x in range(k.value)]
+
     def close(self):
         if getattr(self, "handle", None):
             lib().dip_model_free(self.handle)
@@ -284,12 +306,19 @@ def interleave(model: Model, ws: Workspace, d_records, count: int, d_results, d_
                                 _ptr(d_peaks), _stream(stream)), "dip_interleave")
 
 
+def memopt(model: Model, ws: Workspace, d_records, count: int, d_sel, d_results, d_peaks=None, stream=None):
+    """f3: per-rank strategy selection (d_sel [count][P][2][n_max] u8 out) and the
+    re-timed scores (results as eval_schedules)."""
+    _check(lib().dip_memopt(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_sel), _ptr(d_results),
+                            _ptr(d_peaks), _stream(stream)), "dip_memopt")
+
+
 def search(model: Model, ws: Workspace, split, seed: int, rounds: int, leaves: int, rollouts: int,
-           alpha: float = 1.0, beta: float = 0.5, threads: int = 0, stream=None) -> dict:
+           alpha: float = 1.0, beta: float = 0.5, threads: int = 0, stream=None, memopt: bool = False) -> dict:
     """f2: MCTS over class orders for a fixed split with batched GPU rollouts.
     Returns dict(found, makespan, score, trace, record (host bytes of the best schedule), ...)."""
     sp = np.ascontiguousarray(np.asarray(split, np.uint8).reshape(-1))
-    prm = _SearchParams(seed & ((1 << 64) - 1), rounds, leaves, rollouts, threads, alpha, beta)
+    prm = _SearchParams(seed & ((1 << 64) - 1), rounds, leaves, rollouts, threads, alpha, beta, 1 if memopt else 0)
     out = _SearchResult()
     rec = np.zeros(model.stride, np.uint8)
     trace = np.zeros(rounds, np.float64)

@@ -1,0 +1,102 @@
+"""GPU f3 (dip_set_strategies / dip_memopt, §5.3) vs the oracle (M1-M4):
+the candidate table of every stage-pair type and width equals oracle.mem_candidates, the per-rank
+selections are identical, and the re-timed scores are identical, on every config (generated
+schedules incl. mutated / deadlocked / malformed ones), at several S and at the bench batch size
+on sampled candidates."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gen.problem import problem_arrays, strategy_menu
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2504_14145_b200 as dip  # noqa: E402
+
+
+def chunk_rows(pb):
+    """(module, layers) stage-pair types of the problem"""
+    out = set()
+    for i, md in enumerate(pb.modules):
+        lay = md.chunk_layers if md.chunk_layers is not None else oracle.chunk_layers(md.L, pb.P, md.K)
+        for v in lay:
+            out.add((i, int(v)))
+    return sorted(out)
+
+
+@pytest.mark.parametrize("name,S", [("toy", 10), ("12B", 10), ("37B", 3), ("T2V", 16), ("94B", 10), ("12B", 2)])
+def test_candidate_table_parity(name, S):
+    pb = gen.make_problem(name)
+    menu = strategy_menu(pb)
+    m = dip.Model(pb, 0)
+    m.set_strategies(menu, S)
+    off = problem_arrays(pb)["tab_off"]
+    f, b, a = menu
+    for i, lay in chunk_rows(pb):
+        for W in range(pb.modules[i].w_max + 1):
+            t = int(off[i]) + W
+            ref = oracle.mem_candidates(f[:, t], b[:, t], a[:, t], lay, S) if lay else [(0, 0, 0)]
+            assert m.strategy_candidates(i, lay, W) == ref, (i, lay, W)
+
+
+def run(pb, cs, S=10):
+    m = dip.Model(pb, 0)
+    m.set_strategies(strategy_menu(pb), S)
+    ws = dip.Workspace(m)
+    s = torch.cuda.current_stream()
+    d_rec = torch.from_numpy(m.encode(cs)).cuda()
+    d_res = torch.empty(cs.count * 24, dtype=torch.uint8, device="cuda")
+    d_pk = torch.empty((cs.count, pb.P), dtype=torch.int32, device="cuda")
+    d_sel = torch.empty(cs.count * pb.P * 2 * pb.n_max, dtype=torch.uint8, device="cuda")
+    dip.memopt(m, ws, d_rec, cs.count, d_sel, d_res, d_pk, stream=s)
+    win = dip.argmin(m, ws, cs.count, stream=s)
+    torch.cuda.synchronize()
+    res = dip.results_view(d_res.cpu().numpy()).copy()
+    return res, d_pk.cpu().numpy().view(np.uint32).copy(), d_sel.cpu().numpy().reshape(cs.count, pb.P, 2, pb.n_max), win
+
+
+def check(pb, cs, S=10, idx=None):
+    res, pk, sel, win = run(pb, cs, S)
+    sub = cs if idx is None else cs.subset(idx)
+    rsel, ref = oracle.memopt(pb, sub, strategy_menu(pb), S=S, threads=16)
+    if idx is not None:
+        res, pk, sel = res[idx], pk[idx], sel[idx]
+    assert np.array_equal(res["status"], ref.status), np.nonzero(res["status"] != ref.status)[0][:8]
+    good = ref.status != oracle.ST_BAD
+    assert np.array_equal(sel[good], rsel[good]), np.nonzero((sel != rsel).any(axis=(1, 2, 3)) & good)[0][:8]
+    assert np.array_equal(res["makespan_ns"], ref.makespan)
+    assert np.array_equal(res["oom_mask"], ref.oom_mask)
+    assert np.array_equal(res["bubble"].view(np.uint64), ref.bubble.view(np.uint64))
+    assert np.array_equal(pk.astype(np.uint64), ref.peaks)
+    if idx is None:
+        best = oracle.argmin(ref.makespan, ref.status)
+        assert win.found == (best >= 0) and (best < 0 or win.global_index == best)
+    return res, sel
+
+
+@pytest.mark.parametrize("name,count", [("toy", 256), ("12B", 256), ("37B", 96), ("T2V", 64), ("94B", 24)])
+def test_memopt_parity(name, count):
+    pb = gen.make_problem(name)
+    cs = gen.generate(pb, 0, count, mode=1 if name == "toy" else 0, p_mutate=0.04, p_bad=0.02)
+    res, sel = check(pb, cs)
+    if name != "toy":
+        assert sel.any()                       # some pairs moved off candidate 0
+
+
+@pytest.mark.parametrize("S", [2, 3, 16])
+def test_memopt_parity_other_S(S):
+    pb = gen.make_problem("12B")
+    cs = gen.generate(pb, 0, 96, p_mutate=0.04, p_bad=0.02)
+    check(pb, cs, S=S)
+
+
+def test_memopt_bench_size_sampled():
+    # the bench's f3 launch shape: 16,384 94B schedules in one call, 12 sampled against the oracle
+    pb = gen.make_problem("94B")
+    cs = gen.generate(pb, 0, 16384, threads=16)
+    idx = [0, 1, 2, 777, 4095, 4096, 8191, 9000, 12345, 16000, 16382, 16383]
+    check(pb, cs, idx=idx)

@@ -33,3 +33,23 @@ def test_search_matches_oracle_trajectory(name, rounds, leaves, rollouts):
     n = int(cs.n[0])
     assert np.array_equal(fb_rows(pb, m, rec[None, :])[0], o["bits"])
     assert g["scored"] == rounds * leaves * rollouts or g["scored"] <= rounds * leaves * rollouts
+
+
+@pytest.mark.parametrize("name,rounds,leaves,rollouts", [("toy", 12, 4, 4), ("12B", 6, 8, 6), ("T2V", 3, 4, 3)])
+def test_search_with_memopt_matches_oracle_trajectory(name, rounds, leaves, rollouts):
+    # every rollout is interleaved (f1) and then memory-optimised (f3) before scoring
+    from gen.problem import strategy_menu
+    pb = gen.make_problem(name)
+    cs = gen.generate(pb, 0, 1, mode=1 if name == "toy" else 0, p_mutate=0, p_bad=0)
+    split = cs.split[0]
+    menu = strategy_menu(pb)
+    m = dip.Model(pb, 0)
+    m.set_strategies(menu, 10)
+    ws = dip.Workspace(m)
+    g = dip.search(m, ws, split, seed=4, rounds=rounds, leaves=leaves, rollouts=rollouts, alpha=1.0, beta=0.5,
+                   stream=torch.cuda.current_stream(), memopt=True)
+    o = oracle.search(pb, split, seed=4, rounds=rounds, leaves=leaves, rollouts=rollouts, alpha=1.0, beta=0.5,
+                      menu=menu, S=10)
+    assert np.array_equal(g["trace"], o["trace"])
+    assert g["makespan"] == o["makespan"] and g["score"] == o["score"]
+    assert np.array_equal(fb_rows(pb, m, g["record"][None, :])[0], o["bits"])

@@ -130,3 +130,24 @@ def test_exhaustive_budget_with_chunk_classes():
     r = oracle.search(pb, split, seed=2, rounds=1200, leaves=100, rollouts=2)
     assert r["makespan"] == best_mk
     assert abs(r["score"] - best_score) == 0.0
+
+
+def test_search_with_memopt_rescores_and_improves_scores():
+    # S3 with M1-M4: the best schedule re-scores through the memory optimisation to the
+    # reported makespan; and a rollout never scores lower than without it (pairs only move to
+    # faster candidates, and the longest path is monotone in stage latency), so the first round,
+    # whose rollouts are the same in both searches, has a best score at least as high
+    from gen.problem import strategy_menu
+    pb = gen.make_problem("12B")
+    cs = gen.generate(pb, 0, 1, p_mutate=0, p_bad=0)
+    menu = strategy_menu(pb)
+    a = oracle.search(pb, cs.split[0], seed=3, rounds=6, leaves=4, rollouts=5)
+    b = oracle.search(pb, cs.split[0], seed=3, rounds=6, leaves=4, rollouts=5, menu=menu, S=10)
+    c = cs.subset([0])
+    c.fwd[0] = b["fwd"]
+    c.bwd[0] = b["bwd"]
+    c.fb[0] = b["bits"]
+    sel, rr = oracle.memopt(pb, c, menu, S=10)
+    assert rr.status[0] == oracle.ST_OK and int(rr.makespan[0]) == b["makespan"]
+    assert (np.diff(b["trace"]) >= 0).all()
+    assert b["trace"][0] >= a["trace"][0] > 0
