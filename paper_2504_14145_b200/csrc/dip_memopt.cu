@@ -12,9 +12,10 @@
 //    pair's backward - its backward position), builds the slack profile of candidate 0 with a
 //    difference array + warp scan, then runs the greedy: every lane proposes its best pair
 //    (largest latency saving per KiB, exact u64 cross-multiplication, ties to the lower p), a
-//    5-step shuffle reduction picks the winner, the lanes subtract its memory step over its range
-//    and refresh the cached range-minimum slack of the pairs that overlap it. A pair whose step no
-//    longer fits is dead for good (slack only decreases). Output: sel[x][r][0][p] / [1][q].
+//    5-step shuffle reduction picks the winner, and only then is the winner's step checked
+//    against the range minimum of the slack (lanes over its points): if it fits the lanes subtract
+//    it, else the pair is blocked for good (the slack never grows), which makes this lazy order
+//    pick exactly the oracle's "best feasible pair". Output: sel[x][r][0][p] / [1][q].
 //  The re-timing with the selected candidates (M4) is the scorer's MODE 3 (dip_kernels.cu).
 #include <cstdint>
 
@@ -157,16 +158,15 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
 
     uint8_t *wa = smem + (size_t)warp * warp_bytes;
     long long *slack = reinterpret_cast<long long *>(wa);                  // [n_max]
-    long long *ms = slack + n_max;                                          // [n_max] cached range-min slack
-    int32_t *cb = reinterpret_cast<int32_t *>(ms + n_max);                  // [n_max] ctab row of pair p
+    uint2 *dd = reinterpret_cast<uint2 *>(slack + n_max);                   // [n_max] next step (saving, KiB)
+    int32_t *cb = reinterpret_cast<int32_t *>(dd + n_max);                  // [n_max] ctab row of pair p
     uint16_t *fw = reinterpret_cast<uint16_t *>(cb + n_max);                // [n_max] forward sequence
     uint16_t *invB = fw + n_max;                                            // segment -> backward position
     uint16_t *bsl = invB + n_max;                                           // slot of the q-th backward
     uint16_t *eP = bsl + n_max;                                             // end of pair p's point range
     uint8_t *cur = reinterpret_cast<uint8_t *>(eP + n_max);                 // selected candidate
     uint8_t *ncand = cur + n_max;
-    uint8_t *dead = ncand + n_max;
-    uint8_t *Mb = dead + n_max;                                             // [nq]
+    uint8_t *Mb = ncand + n_max;                                            // [nq]
 
     const long long INF = 0x7FFFFFFFFFFFFFFFll;
     for (;;) {
@@ -260,7 +260,6 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 const uint4 E = __ldg(&kp.ctab[row]);
                 ncand[p] = (uint8_t)E.w;
                 cur[p] = 0;
-                dead[p] = 0;
                 if (e > p) {
                     atomicAdd(reinterpret_cast<unsigned long long *>(&slack[p]), (unsigned long long)E.z);
                     if (e < n) atomicAdd(reinterpret_cast<unsigned long long *>(&slack[e]), (unsigned long long)(-(long long)E.z));
@@ -295,21 +294,27 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             __syncwarp();
         }
         if (feasible) {
+            // dd[p] = (latency saving, memory step) of pair p's next candidate; step 0 = none left
             for (uint32_t p = lane; p < n; p += 32) {
-                long long mn = INF;
-                for (uint32_t k = p; k < eP[p]; k++) mn = slack[k] < mn ? slack[k] : mn;
-                ms[p] = mn;
+                uint2 d = make_uint2(0u, 0u);
+                if (ncand[p] > 1) {
+                    const uint4 E0 = __ldg(&kp.ctab[cb[p]]), E1 = __ldg(&kp.ctab[cb[p] + 1]);
+                    d = make_uint2((E0.x + E0.y) - (E1.x + E1.y), E1.z - E0.z);
+                }
+                dd[p] = d;
             }
             __syncwarp();
             for (;;) {
-                // each lane's best upgrade: max dl/dm, ties to the lower p
-                uint32_t bdl = 0, bdm = 1, bp = 0xFFFFFFFFu;
+                // the pair with the largest saving per KiB (ties to the lower p) among those not yet
+                // known to be blocked; its feasibility is checked only now (lazily): a pair whose step
+                // does not fit is blocked for good, because the slack never grows
+                uint32_t bdl = 0, bdm = 0, bp = 0xFFFFFFFFu;
                 for (uint32_t p = lane; p < n; p += 32) {
-                    if (dead[p] || cur[p] + 1u >= ncand[p]) continue;
-                    const uint4 E0 = __ldg(&kp.ctab[cb[p] + cur[p]]), E1 = __ldg(&kp.ctab[cb[p] + cur[p] + 1]);
-                    const uint32_t dm = E1.z - E0.z, dl = (E0.x + E0.y) - (E1.x + E1.y);
-                    if ((long long)dm > ms[p]) { dead[p] = 1; continue; }
-                    if (bp == 0xFFFFFFFFu || (unsigned long long)dl * bdm > (unsigned long long)bdl * dm) { bdl = dl; bdm = dm; bp = p; }
+                    const uint2 d = dd[p];
+                    if (d.y == 0) continue;
+                    if (bp == 0xFFFFFFFFu || (unsigned long long)d.x * bdm > (unsigned long long)bdl * d.y) {
+                        bdl = d.x; bdm = d.y; bp = p;
+                    }
                 }
                 for (int o = 16; o > 0; o >>= 1) {
                     const uint32_t ol = __shfl_xor_sync(FULL, bdl, o), om = __shfl_xor_sync(FULL, bdm, o),
@@ -325,16 +330,28 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 }
                 if (bp == 0xFFFFFFFFu) break;
                 const uint32_t a0 = bp, a1 = eP[bp];
+                long long mn = INF;
+                for (uint32_t k = a0 + lane; k < a1; k += 32) mn = slack[k] < mn ? slack[k] : mn;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const long long v = __shfl_xor_sync(FULL, mn, o);
+                    mn = v < mn ? v : mn;
+                }
                 __syncwarp();
-                if (lane == 0) cur[a0] = (uint8_t)(cur[a0] + 1);
+                if ((long long)bdm > mn) {                 // blocked for good
+                    if (lane == 0) dd[a0] = make_uint2(0u, 0u);
+                    __syncwarp();
+                    continue;
+                }
                 for (uint32_t k = a0 + lane; k < a1; k += 32) slack[k] -= (long long)bdm;
-                __syncwarp();
-                for (uint32_t p = lane; p < n; p += 32) {   // refresh the range minimum where it overlaps
-                    const uint32_t lo = p > a0 ? p : a0, hi = eP[p] < a1 ? eP[p] : a1;
-                    if (lo >= hi) continue;
-                    long long mn = ms[p];
-                    for (uint32_t k = lo; k < hi; k++) mn = slack[k] < mn ? slack[k] : mn;
-                    ms[p] = mn;
+                if (lane == 0) {
+                    const uint32_t c = cur[a0] + 1u;
+                    cur[a0] = (uint8_t)c;
+                    uint2 d = make_uint2(0u, 0u);
+                    if (c + 1u < ncand[a0]) {
+                        const uint4 E0 = __ldg(&kp.ctab[cb[a0] + c]), E1 = __ldg(&kp.ctab[cb[a0] + c + 1]);
+                        d = make_uint2((E0.x + E0.y) - (E1.x + E1.y), E1.z - E0.z);
+                    }
+                    dd[a0] = d;
                 }
                 __syncwarp();
             }
