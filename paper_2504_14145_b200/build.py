@@ -29,12 +29,13 @@ def _nccl_dirs():
     return None, None
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in DEPS):
-        return SO
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = SO) -> str:
+    """Build libdip.so (or, with `defines` / `out`, a variant library for kernel A/B runs)."""
+    if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in DEPS):
+        return out
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
-           *SRCS, "-o", SO]
+           *[f"-D{d}" for d in defines], *SRCS, "-o", out]
     inc, lib = _nccl_dirs()
     if inc:
         cmd[1:1] = ["-I", inc]
@@ -44,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    return SO
+    return out
 
 
 if __name__ == "__main__":

@@ -100,6 +100,7 @@ constexpr uint32_t E_MULTI = 4u << 24;    // several join targets: slower loop (
 //   slot = max(slot, (slot & HIGH) | value) + (1 << 56)
 constexpr uint64_t HIGH_MASK = ~VAL_MASK;
 
+
 // rare paths kept out of line (a call is never if-converted into the round's common path)
 __device__ __noinline__ uint64_t spill_load(const unsigned long long *spill, uint32_t d, uint32_t r, uint32_t P,
                                             uint32_t n_max, uint32_t idx) {
@@ -338,25 +339,26 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         // Per round every lane of the group tries its next slot (F if bit t is 0, else B):
         // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
         // P-1 for B, from a wrap slot), end = max(t_last, dep + p2p) + layers * lat, then publish
-        // end into its own channel ring (or read-modify-write a wrap slot). The F and B state is
-        // indexed by isB with shifts (counts packed as fi | bi << 16) rather than selects.
+        // end into its own channel ring (or read-modify-write a wrap slot). The neighbours' F and B
+        // counts travel as four separate shuffles (the shuffle unit is idle; the ALU pipe is the
+        // bottleneck, so no packing / unpacking). Exit and cycle checks run every 8th round.
         // Channel rings are [2][D][P] u64 (F rings, then B rings; lane x owns column x).
         bool done = bad || !laneOn || n == 0;
-        uint32_t t = 0, cnt = 0;                 // cnt = fi | bi << 16
+        uint32_t t = 0, cF = 0, cB = 0;          // forward / backward stages placed so far
+        uint32_t rnd = 0;
         const uint32_t *wptr = reinterpret_cast<const uint32_t *>(rec + kp.off_fb) + 2 * P + r;   // word 2 of this row
         const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
         const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
         const uint32_t wrapBits = (isFirst ? 1u : 0u) | (isLast ? 2u : 0u);   // bit d: consumes dir d via wrap
         const uint32_t wrapPub = (isLast ? 1u : 0u) | (isFirst ? 2u : 0u);    // bit d: publishes dir d via wrap
         for (;;) {
-            const uint32_t up = __shfl_up_sync(FULL, cnt, 1, G);
-            const uint32_t dn = __shfl_down_sync(FULL, cnt, 1, G);
             const uint32_t d = (wcur >> (t & 31)) & 1u;            // 0 = F, 1 = B
-            const uint32_t sh = d << 4;
-            const uint32_t idx = (cnt >> sh) & 0xFFFFu;
             const bool wrapC = (wrapBits >> d) & 1u;
             const bool wrapP = (wrapPub >> d) & 1u;
-            const uint32_t nb = wrapC ? 0xFFFFu : (((d ? dn : up) >> sh) & 0xFFFFu);   // producer's count
+            const uint32_t fu = __shfl_up_sync(FULL, cF, 1, G), bu = __shfl_up_sync(FULL, cB, 1, G);
+            const uint32_t fd = __shfl_down_sync(FULL, cF, 1, G), bd = __shfl_down_sync(FULL, cB, 1, G);
+            const uint32_t idx = d ? cB : cF;
+            const uint32_t nb = wrapC ? 0xFFFFu : (d ? bd : fu);                        // producer's count
             const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];       // done lanes: a safe row
             const uint32_t ring = (idx & (D - 1)) * P;
             const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (d ? colIn1 : colIn0)];
@@ -365,18 +367,23 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             const uint32_t lay = layers[((e.x >> 12) & 0xFFFu) + r];
             const uint64_t v = *ca;
             const uint64_t pold = *pa;
-            const bool ready = !done && nb > idx && (v >> PEND_SHIFT) == 0;
+            // a ready value has a zero pending byte, so it needs no mask (v < 2^56 <=> high word < 2^24)
+            const bool ready = !done && nb > idx && (uint32_t)(v >> 32) < (1u << 24);
             const uint32_t w = (wrapC && !d) ? 0u : T.w;   // rank 0's F wrap slot already holds + p2p
-            uint64_t dep = (v + w) & VAL_MASK;
+            uint64_t dep = v + w;
             if (ready && !wrapC && idx + D < nb)   // evicted from the channel ring: exact spill copy
                 dep = spill_load(spill, d, r, P, n_max, idx) + w;
 
-            const uint32_t prog = __ballot_sync(FULL, ready);
-            const uint32_t alive = __ballot_sync(FULL, !done);
-            if (alive == 0) break;
-            if ((alive & gmask) && !(prog & gmask)) {   // no lane of this group can move: a cycle
-                dl = true;
-                done = true;
+            // exit / cycle checks every 8th round: a round without progress repeats forever, so the
+            // verdict is exact; finished lanes just idle for at most 7 rounds
+            if ((++rnd & 7) == 0) {
+                const uint32_t prog = __ballot_sync(FULL, ready);
+                const uint32_t alive = __ballot_sync(FULL, !done);
+                if (alive == 0) break;
+                if ((alive & gmask) && !(prog & gmask)) {   // no lane of this group can move: a cycle
+                    dl = true;
+                    done = true;
+                }
             }
             __syncwarp();
             if (ready) {
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 const uint64_t rmw = (cand > pold ? cand : pold) + (1ull << PEND_SHIFT);
                 *pa = wrapP ? rmw : end;
                 if (!wrapP) {
-                    const uint32_t cc = ((d ? up : dn) >> sh) & 0xFFFFu;   // consumer neighbour's count
+                    const uint32_t cc = d ? bu : fd;                       // consumer neighbour's count
                     if (idx >= cc + D)                    // consumer is >= D behind: keep the old entry
                         spill_keep(spill, d, r, P, n_max, idx, pold);
                 } else if (e.x & E_MULTI) {               // several join targets (rare); the plain store hit SINK
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                         *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
                     }
                 }
-                cnt += 1u << sh;
+                if (d) cB++; else cF++;
                 t++;
                 if ((t & 31) == 0) {                      // next 32 F/B bits: the word after next is prefetched
                     wcur = wnext;
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
             __syncwarp();
         }
-        uint32_t fi = cnt & 0xFFFFu, bi = cnt >> 16;
+        uint32_t fi = cF, bi = cB;
         // deadlocked candidates: finish the order-only memory scan (R-9)
         if (dl && laneOn) {
             while (t < S2) {

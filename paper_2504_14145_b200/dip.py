@@ -89,10 +89,11 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"{LIB_PATH} is missing: run `python paper_2504_14145_b200/build.py` "
+    path = os.environ.get("DIP_LIB", LIB_PATH)     # an alternative in-tree build (kernel A/B runs)
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: run `python paper_2504_14145_b200/build.py` "
                            "(there is no CPU fallback for the scoring path)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     st = ctypes.c_int
     vp = ctypes.c_void_p
     L.dip_load_cost_model.argtypes = [ctypes.POINTER(_ProblemDesc), ctypes.c_int, ctypes.POINTER(vp)]
