@@ -295,6 +295,7 @@ dip_status dip_model_free(dip_model *m) {
     if (m->d_blob) cudaFree(m->d_blob);
     if (m->d_ctab) cudaFree(m->d_ctab);
     if (m->d_crow) cudaFree(m->d_crow);
+    if (m->d_srank) cudaFree(m->d_srank);
     delete m;
     return DIP_OK;
 }

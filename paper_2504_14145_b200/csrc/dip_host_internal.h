@@ -62,6 +62,7 @@ struct dip_model {
     std::vector<uint4> h_ctab;                    // host copy of the candidate table
     uint4 *d_ctab = nullptr;
     int32_t *d_crow = nullptr;
+    uint16_t *d_srank = nullptr;
     uint32_t mo_warp_bytes = 0;
     int mo_grid = 0;
 };

@@ -42,6 +42,7 @@ struct KParams {
     const uint8_t *sel;         // non-null: f3 mode, [count][P][2][n_max] selected candidate per stage pair
     const uint4 *ctab;          // f3 candidates {F ns, B ns, act KiB, count} per (type, W, c)
     const int32_t *crow;        // f3: per chunk row, ctab base of its (module, layers) type - tab_off * S
+    const uint16_t *srank;      // f3: per ctab entry c, the rank of the step c -> c+1 by saving per KiB
     uint32_t S;                 // f3: candidates per (type, W)
     uint64_t count, index_base;
     dip_result *results;

@@ -11,8 +11,9 @@
 //    position p -> its point range [p, e_p) over the rank's forward slots, e_p = slot of the
 //    pair's backward - its backward position), builds the slack profile of candidate 0 with a
 //    difference array + warp scan, then runs the greedy: every lane proposes its best pair
-//    (largest latency saving per KiB, exact u64 cross-multiplication, ties to the lower p), a
-//    5-step shuffle reduction picks the winner, and only then is the winner's step checked
+//    (largest latency saving per KiB, ties to the lower p, as a 32-bit key built from the host's
+//    exact ranking of all steps of the candidate table), one REDUX picks the winner, and only
+//    then is the winner's step checked
 //    against the range minimum of the slack (lanes over its points): if it fits the lanes subtract
 //    it, else the pair is blocked for good (the slack never grows), which makes this lazy order
 //    pick exactly the oracle's "best feasible pair". Output: sel[x][r][0][p] / [1][q].
@@ -157,18 +158,20 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
     const uint32_t *budget = reinterpret_cast<const uint32_t *>(kp.blob + kp.b_budget);
 
     uint8_t *wa = smem + (size_t)warp * warp_bytes;
-    long long *slack = reinterpret_cast<long long *>(wa);                  // [n_max]
-    uint2 *dd = reinterpret_cast<uint2 *>(slack + n_max);                   // [n_max] next step (saving, KiB)
+    int32_t *slack = reinterpret_cast<int32_t *>(wa);                      // [n_max] (|values| < 2^31: host guard)
+    uint2 *dd = reinterpret_cast<uint2 *>(wa + 4 * ((n_max + 1) & ~1u));  // [n_max] next step (saving, KiB)
+    uint16_t *fw = reinterpret_cast<uint16_t *>(dd);                        // decode scratch, dead before dd is
+    uint16_t *invB = fw + n_max;                                            //   written: forward sequence,
+    uint16_t *bsl = invB + n_max;                                           //   segment -> backward position,
+                                                                            //   slot of the q-th backward
     int32_t *cb = reinterpret_cast<int32_t *>(dd + n_max);                  // [n_max] ctab row of pair p
-    uint16_t *fw = reinterpret_cast<uint16_t *>(cb + n_max);                // [n_max] forward sequence
-    uint16_t *invB = fw + n_max;                                            // segment -> backward position
-    uint16_t *bsl = invB + n_max;                                           // slot of the q-th backward
-    uint16_t *eP = bsl + n_max;                                             // end of pair p's point range
-    uint8_t *cur = reinterpret_cast<uint8_t *>(eP + n_max);                 // selected candidate
+    uint16_t *eP = reinterpret_cast<uint16_t *>(cb + n_max);                // end of pair p's point range
+    uint16_t *qp = eP + n_max;                                              // backward position of pair p
+    uint8_t *cur = reinterpret_cast<uint8_t *>(qp + n_max);                 // selected candidate
     uint8_t *ncand = cur + n_max;
     uint8_t *Mb = ncand + n_max;                                            // [nq]
 
-    const long long INF = 0x7FFFFFFFFFFFFFFFll;
+    const int32_t INF = 0x7FFFFFFF;
     for (;;) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(kp.counter, 1ull);
@@ -251,6 +254,7 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 if (q == 0xFFFFu) { bad = true; continue; }
                 const uint32_t e = (uint32_t)bsl[q] - q;
                 eP[p] = (uint16_t)e;
+                qp[p] = (uint16_t)q;
                 const uint32_t dc = __ldg(&segdec[s]);
                 const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
                 const uint32_t qq = b * nmod + i, M = Mb[qq];
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 ncand[p] = (uint8_t)E.w;
                 cur[p] = 0;
                 if (e > p) {
-                    atomicAdd(reinterpret_cast<unsigned long long *>(&slack[p]), (unsigned long long)E.z);
-                    if (e < n) atomicAdd(reinterpret_cast<unsigned long long *>(&slack[e]), (unsigned long long)(-(long long)E.z));
+                    atomicAdd(&slack[p], (int32_t)E.z);
+                    if (e < n) atomicSub(&slack[e], (int32_t)E.z);
                 }
             }
             bad = __any_sync(FULL, bad);
@@ -273,15 +277,15 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             continue;
         }
         // prefix sum -> slack = budget - used at every forward slot
-        const long long bud = (long long)__ldg(&budget[r]);
+        const int32_t bud = (int32_t)__ldg(&budget[r]);
         bool feasible = true;
         {
-            long long run = 0;
+            int32_t run = 0;
             for (uint32_t k0 = 0; k0 < n; k0 += 32) {
                 const uint32_t k = k0 + lane;
-                long long v = k < n ? slack[k] : 0;
+                int32_t v = k < n ? slack[k] : 0;
                 for (int o = 1; o < 32; o <<= 1) {
-                    const long long u = __shfl_up_sync(FULL, v, o);
+                    const int32_t u = __shfl_up_sync(FULL, v, o);
                     if (lane >= o) v += u;
                 }
                 if (k < n) {
@@ -294,62 +298,45 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             __syncwarp();
         }
         if (feasible) {
-            // dd[p] = (latency saving, memory step) of pair p's next candidate; step 0 = none left
+            // key[p] = (0xFFFF - rank of pair p's next step) << 16 | (0xFFFF - p), 0 = none left:
+            // the host ranks every step of the candidate table by its exact latency saving per KiB
+            // (equal ratios share a rank), so the warp max of the keys is the oracle's choice --
+            // largest ratio, ties to the lower p -- in one REDUX instead of a cross-multiplied
+            // shuffle tournament
             for (uint32_t p = lane; p < n; p += 32) {
-                uint2 d = make_uint2(0u, 0u);
+                uint32_t key = 0, dm = 0;
                 if (ncand[p] > 1) {
-                    const uint4 E0 = __ldg(&kp.ctab[cb[p]]), E1 = __ldg(&kp.ctab[cb[p] + 1]);
-                    d = make_uint2((E0.x + E0.y) - (E1.x + E1.y), E1.z - E0.z);
+                    key = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[p]])) << 16) | (0xFFFFu - p);
+                    dm = __ldg(&kp.ctab[cb[p] + 1]).z - __ldg(&kp.ctab[cb[p]]).z;
                 }
-                dd[p] = d;
+                dd[p] = make_uint2(key, dm);
             }
             __syncwarp();
             for (;;) {
-                // the pair with the largest saving per KiB (ties to the lower p) among those not yet
-                // known to be blocked; its feasibility is checked only now (lazily): a pair whose step
-                // does not fit is blocked for good, because the slack never grows
-                uint32_t bdl = 0, bdm = 0, bp = 0xFFFFFFFFu;
-                for (uint32_t p = lane; p < n; p += 32) {
-                    const uint2 d = dd[p];
-                    if (d.y == 0) continue;
-                    if (bp == 0xFFFFFFFFu || (unsigned long long)d.x * bdm > (unsigned long long)bdl * d.y) {
-                        bdl = d.x; bdm = d.y; bp = p;
-                    }
-                }
-                for (int o = 16; o > 0; o >>= 1) {
-                    const uint32_t ol = __shfl_xor_sync(FULL, bdl, o), om = __shfl_xor_sync(FULL, bdm, o),
-                                   op = __shfl_xor_sync(FULL, bp, o);
-                    bool take;
-                    if (op == 0xFFFFFFFFu) take = false;
-                    else if (bp == 0xFFFFFFFFu) take = true;
-                    else {
-                        const unsigned long long a = (unsigned long long)ol * bdm, c = (unsigned long long)bdl * om;
-                        take = a > c || (a == c && op < bp);
-                    }
-                    if (take) { bdl = ol; bdm = om; bp = op; }
-                }
-                if (bp == 0xFFFFFFFFu) break;
-                const uint32_t a0 = bp, a1 = eP[bp];
-                long long mn = INF;
-                for (uint32_t k = a0 + lane; k < a1; k += 32) mn = slack[k] < mn ? slack[k] : mn;
-                for (int o = 16; o > 0; o >>= 1) {
-                    const long long v = __shfl_xor_sync(FULL, mn, o);
-                    mn = v < mn ? v : mn;
-                }
+                // the best pair not yet known to be blocked; its feasibility is checked only now
+                // (lazily): a pair whose step does not fit is blocked for good (the slack never grows)
+                uint32_t best = 0;
+                for (uint32_t p = lane; p < n; p += 32) best = max(best, dd[p].x);
+                best = __reduce_max_sync(FULL, best);
+                if (best == 0) break;
+                const uint32_t a0 = 0xFFFFu - (best & 0xFFFFu), a1 = eP[a0], bdm = dd[a0].y;
+                int32_t mn = INF;
+                for (uint32_t k = a0 + lane; k < a1; k += 32) mn = min(mn, slack[k]);
+                mn = __reduce_min_sync(FULL, mn);
                 __syncwarp();
-                if ((long long)bdm > mn) {                 // blocked for good
+                if ((int64_t)bdm > (int64_t)mn) {          // blocked for good
                     if (lane == 0) dd[a0] = make_uint2(0u, 0u);
                     __syncwarp();
                     continue;
                 }
-                for (uint32_t k = a0 + lane; k < a1; k += 32) slack[k] -= (long long)bdm;
+                for (uint32_t k = a0 + lane; k < a1; k += 32) slack[k] -= (int32_t)bdm;
                 if (lane == 0) {
                     const uint32_t c = cur[a0] + 1u;
                     cur[a0] = (uint8_t)c;
                     uint2 d = make_uint2(0u, 0u);
                     if (c + 1u < ncand[a0]) {
-                        const uint4 E0 = __ldg(&kp.ctab[cb[a0] + c]), E1 = __ldg(&kp.ctab[cb[a0] + c + 1]);
-                        d = make_uint2((E0.x + E0.y) - (E1.x + E1.y), E1.z - E0.z);
+                        d.x = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[a0] + c])) << 16) | (0xFFFFu - a0);
+                        d.y = __ldg(&kp.ctab[cb[a0] + c + 1]).z - __ldg(&kp.ctab[cb[a0] + c]).z;
                     }
                     dd[a0] = d;
                 }
@@ -359,7 +346,7 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
         for (uint32_t p = lane; p < n_max; p += 32) {
             const uint8_t c = p < n ? cur[p] : 0;
             selF[p] = c;
-            if (p < n) selB[invB[fw[p]]] = c;
+            if (p < n) selB[qp[p]] = c;
         }
         if (n < n_max)
             for (uint32_t q = n + lane; q < n_max; q += 32) selB[q] = 0;

@@ -111,8 +111,50 @@ extern "C" dip_status dip_set_strategies(dip_model *M, uint32_t n_strat, const u
             }
         }
     }
+    {   // the selection keeps slack in int32: budget and the live memory must stay below 2^31 KiB
+        uint64_t maxmem = 0, maxbud = 0;
+        for (size_t x = 0; x < h.size(); x++) maxmem = std::max<uint64_t>(maxmem, h[x].z);
+        const uint32_t *bud = reinterpret_cast<const uint32_t *>(M->blob.data() + M->kp.b_budget);
+        for (uint32_t r = 0; r < P; r++) maxbud = std::max<uint64_t>(maxbud, bud[r]);
+        if (maxbud >= (1ull << 31) || (unsigned __int128)maxmem * M->n_max + maxbud >= ((unsigned __int128)1 << 31)) {
+            cudaFree(d_ctab); cudaFree(d_crow);
+            return fail(DIP_ERANGE, "budget / live memory of a rank may exceed 2^31 KiB");
+        }
+    }
+    // exact ranking of every step c -> c+1 by latency saving per KiB (equal ratios share a rank):
+    // the selection kernel then compares 32-bit keys (rank, pair) instead of cross-multiplying
+    std::vector<uint16_t> srank(base, 0xFFFFu);
+    {
+        struct Step { uint64_t dl, dm; uint32_t at; };
+        std::vector<Step> steps;
+        for (size_t row = 0; row < base; row += S)
+            for (uint32_t c = 0; c + 1 < h[row].w; c++) {
+                const uint4 &a = h[row + c], &b = h[row + c + 1];
+                steps.push_back({(uint64_t)a.x + a.y - ((uint64_t)b.x + b.y), (uint64_t)b.z - a.z, (uint32_t)(row + c)});
+            }
+        auto better = [](const Step &x, const Step &y) {
+            return (unsigned __int128)x.dl * y.dm > (unsigned __int128)y.dl * x.dm;
+        };
+        std::stable_sort(steps.begin(), steps.end(), better);
+        uint32_t rank = 0;
+        for (size_t x = 0; x < steps.size(); x++) {
+            if (x > 0 && better(steps[x - 1], steps[x])) rank++;
+            if (rank >= 0xFFFFu) { cudaFree(d_ctab); cudaFree(d_crow); return fail(DIP_ERANGE, "more than 65534 distinct step ratios"); }
+            srank[steps[x].at] = (uint16_t)rank;
+        }
+    }
+    uint16_t *d_srank = nullptr;
+    if (cudaMalloc(&d_srank, srank.size() * 2 + 2) != cudaSuccess ||
+        cudaMemcpy(d_srank, srank.data(), srank.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d_ctab); cudaFree(d_crow);
+        if (d_srank) cudaFree(d_srank);
+        return fail(DIP_ECUDA, "step ranks");
+    }
     if (M->d_ctab) cudaFree(M->d_ctab);
     if (M->d_crow) cudaFree(M->d_crow);
+    if (M->d_srank) cudaFree(M->d_srank);
+    M->d_srank = d_srank;
+    M->kp.srank = d_srank;
     M->d_ctab = d_ctab;
     M->d_crow = d_crow;
     M->h_ctab.swap(h);
@@ -124,7 +166,7 @@ extern "C" dip_status dip_set_strategies(dip_model *M, uint32_t n_strat, const u
     M->kp.S = S;
     // selection kernel shape: 4 warps per block, per-warp working set in shared memory
     const uint32_t nmx = M->n_max, nq = M->m * nm;
-    M->mo_warp_bytes = up16(nmx * (8 + 8 + 4 + 2 + 2 + 2 + 2 + 1 + 1) + nq);
+    M->mo_warp_bytes = up16(4 * ((nmx + 1) & ~1u) + nmx * (8 + 4 + 2 + 2 + 1 + 1) + nq);
     const size_t smem = 4 * (size_t)M->mo_warp_bytes;
     cudaDeviceProp prop;
     CUDA_TRY(cudaGetDeviceProperties(&prop, M->device));
