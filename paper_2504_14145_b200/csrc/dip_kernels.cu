@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         // lowest rank) and that rank places one stage: alternating F/B when both heads are
         // ready before t_last, else the smaller t_start (ties to B, R-29). If every rank
         // is blocked by its gate only, the gate is lifted for one step (R-31).
-        uint32_t cnt = 0, wbuf = 0;
+        uint32_t fi = 0, bi = 0, wbuf = 0;      // forward / backward stages placed so far
         int last = -1;
         bool done = bad || !laneOn || n == 0;
         uint32_t *fbOut = reinterpret_cast<uint32_t *>(kp.records_out + (gvalid ? cand : 0) * (uint64_t)kp.stride + kp.off_fb) + r;
@@ -473,28 +473,27 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
         const uint32_t bud = budget[laneOn ? r : 0];
         for (;;) {
-            const uint32_t up = __shfl_up_sync(FULL, cnt, 1, G);
-            const uint32_t dn = __shfl_down_sync(FULL, cnt, 1, G);
-            const uint32_t fi = cnt & 0xFFFFu, bi = cnt >> 16;
+            const uint32_t fu = __shfl_up_sync(FULL, fi, 1, G), bu = __shfl_up_sync(FULL, bi, 1, G);
+            const uint32_t fd = __shfl_down_sync(FULL, fi, 1, G), bd = __shfl_down_sync(FULL, bi, 1, G);
             const bool hasF = !done && fi < n, hasB = !done && bi < n;
             // forward head
             const uint2 eF = hasF ? posAll[fi] : make_uint2(0u, 0u);
             const uint4 TF = tab[eF.x & 0xFFFu];
             const uint32_t layF = layers[((eF.x >> 12) & 0xFFFu) + r];
-            const uint32_t nbF = up & 0xFFFFu;
+            const uint32_t nbF = fu;
             uint64_t vF = hasF ? (isFirst ? depAll[eF.y & 0xFFFFu] : ringAll[(fi & (D - 1)) * P + colIn0]) : 0ull;
-            const bool rdyF = hasF && (isFirst ? (vF >> PEND_SHIFT) == 0 : nbF > fi);
+            const bool rdyF = hasF && (isFirst ? (uint32_t)(vF >> 32) < (1u << 24) : nbF > fi);
             if (rdyF && !isFirst && fi + D < nbF) vF = spill_load(spill, 0, r, P, n_max, fi);
-            const uint64_t tF = (vF + (isFirst ? 0u : TF.w)) & VAL_MASK;
+            const uint64_t tF = vF + (isFirst ? 0u : TF.w);   // used only when ready (pending byte 0)
             // backward head
             const uint2 eB = hasB ? posAll[n_max + bi] : make_uint2(0u, 0u);
             const uint4 TB = tab[eB.x & 0xFFFu];
             const uint32_t layB = layers[((eB.x >> 12) & 0xFFFu) + r];
-            const uint32_t nbB = dn >> 16;
+            const uint32_t nbB = bd;
             uint64_t vB = hasB ? (isLast ? depAll[eB.y & 0xFFFFu] : ringAll[(bi & (D - 1)) * P + colIn1]) : 0ull;
-            const bool rdyB = hasB && (isLast ? (vB >> PEND_SHIFT) == 0 : nbB > bi);
+            const bool rdyB = hasB && (isLast ? (uint32_t)(vB >> 32) < (1u << 24) : nbB > bi);
             if (rdyB && !isLast && bi + D < nbB) vB = spill_load(spill, 1, r, P, n_max, bi);
-            const uint64_t tB = (vB + TB.w) & VAL_MASK;
+            const uint64_t tB = vB + TB.w;
             // memory gate and the group's argmin of (t_min, rank)
             const uint32_t actF = layF * TF.z;
             const bool gated = rdyF && cur + actF > bud;
@@ -545,7 +544,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 const uint64_t cand2 = (pold & HIGH_MASK) | pv;
                 *pa = wrapP ? (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT) : end;
                 if (!wrapP) {
-                    const uint32_t ccnt = dir ? (up >> 16) : (dn & 0xFFFFu);   // consumer neighbour's count
+                    const uint32_t ccnt = dir ? bu : fd;                     // consumer neighbour's count
                     if (idx >= ccnt + D) spill_keep(spill, dir, r, P, n_max, idx, pold);
                 } else if (e.x & E_MULTI) {
                     const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
@@ -561,14 +560,14 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 const uint32_t t = fi + bi;
                 if (dir) wbuf |= 1u << (t & 31);
                 if ((t & 31) == 31 || t + 1 == S2) { fbOut[(t >> 5) * P] = wbuf; wbuf = 0; }
-                cnt += dir ? 0x10000u : 1u;
+                if (dir) bi++; else fi++;
                 last = (int)dir;
                 done = t + 1 == S2;
             }
             __syncwarp();
         }
         if (dl && laneOn && wbuf) {                        // flush the partial word of a deadlocked build
-            const uint32_t t = (cnt & 0xFFFFu) + (cnt >> 16);
+            const uint32_t t = fi + bi;
             fbOut[(t >> 5) * P] = wbuf;
         }
         }
