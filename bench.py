@@ -113,9 +113,16 @@ def cpu_baseline(pb, cs, sample: int, threads: int, core_seconds: float = 20.0):
     t0 = time.perf_counter()
     oracle.evaluate(pb, sub, threads=threads)
     dt = time.perf_counter() - t0
+    # and on ONE core (report the ratio against both), over ~5 s of work
+    one = cs.subset(np.arange(min(cs.count, max(64, int(5.0 / max(per_cand, 1e-7))))))
+    t1 = time.perf_counter()
+    oracle.evaluate(pb, one, threads=1)
+    d1 = time.perf_counter() - t1
     return {"value": sub.count / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"first {sub.count} candidates of rank 0's shard ({dt:.1f} s wall, "
-                      f"{dt * threads:.0f} core-s)"}
+                      f"{dt * threads:.0f} core-s)",
+            "one_core": {"value": one.count / d1, "unit": UNIT, "cores": 1,
+                         "sample": f"first {one.count} candidates ({d1:.1f} s)"}}
 
 
 def run_reference(args, rank, world):
@@ -274,8 +281,15 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         assert w2.global_index == win.global_index and w2.makespan_ns == win.makespan_ns
+        # the copy alone: what bounds the end-to-end number when it is below the device number
+        a.record(stream)
+        d_rec.copy_(h_rec, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        h2d = per * model.stride / (a.elapsed_time(b) / 1e3) / 1e9
         e2e = {"value": per * world * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": per * model.stride, "d2h_bytes_per_step": 8,
+               "h2d_GBps_alone": h2d,
                "path": "dip_eval_host: pinned host records, 64K-record chunks, H2D overlapped with scoring"}
 
     # ---- DIP's dual-queue interleaving on the first f1-count records

@@ -100,3 +100,34 @@ def test_memopt_bench_size_sampled():
     cs = gen.generate(pb, 0, 16384, threads=16)
     idx = [0, 1, 2, 777, 4095, 4096, 8191, 9000, 12345, 16000, 16382, 16383]
     check(pb, cs, idx=idx)
+
+
+def test_strategy_menu_guards():
+    import copy
+    pb = gen.make_problem("12B")
+    f, b, a = strategy_menu(pb)
+    m = dip.Model(pb, 0)
+    ws = dip.Workspace(m)
+    d = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(dip.DipError) as e:            # no menu yet
+        dip.memopt(m, ws, d, 1, d, d, None)
+    assert e.value.code == 1
+    for S in (1, 17):                                  # S out of range
+        with pytest.raises(dip.DipError) as e:
+            m.set_strategies((f, b, a), S)
+        assert e.value.code == 1
+    # a second strategy with the same memory and latency but another F/B split: two non-dominated
+    # candidates of equal memory, which the strict selection order cannot rank
+    f1 = np.where(b[0] > 0, f[0] + 1, f[0]).astype(np.uint32)
+    b1 = np.where(b[0] > 0, b[0] - 1, b[0]).astype(np.uint32)
+    with pytest.raises(dip.DipError) as e:
+        m.set_strategies((np.stack([f[0], f1]), np.stack([b[0], b1]), np.stack([a[0], a[0]])), 10)
+    assert e.value.code == 4
+    pb2 = copy.deepcopy(pb)                            # budgets beyond the int32 selection
+    pb2.budget_kib = np.full(pb.P, (1 << 31) + 5, np.uint32)
+    m2 = dip.Model(pb2, 0)
+    with pytest.raises(dip.DipError) as e:
+        m2.set_strategies((f, b, a), 10)
+    assert e.value.code == 4
+    m.set_strategies((f, b, a), 10)                    # and a valid menu still loads afterwards
+    assert m.strategy_candidates(1, oracle.chunk_layers(pb.modules[1].L, pb.P, pb.modules[1].K)[0], 5)
