@@ -137,8 +137,10 @@ typedef struct {
 } dip_result;
 
 /* Per-stream scratch: work-queue counter, fused argmin key, spill area for the
- * DP's inter-rank channels, and (if host_chunk > 0) double-buffered device
- * staging of host_chunk records for dip_eval_host. */
+ * DP's inter-rank channels, and (if host_chunk > 0) the dip_eval_host pipeline:
+ * three device staging buffers of host_chunk records, a copy stream, a second
+ * compute stream with its own spill area (chunks alternate between the caller's
+ * stream and it, so one chunk's tail overlaps the next chunk's start). */
 dip_status dip_workspace_create(const dip_model *m, size_t host_chunk, dip_workspace **out);
 dip_status dip_workspace_free(dip_workspace *w);
 

@@ -380,13 +380,17 @@ dip_status dip_workspace_create(const dip_model *M, size_t host_chunk, dip_works
     CUDA_TRY(cudaMalloc(&w->d_spill, w->spill_bytes));
     w->host_chunk = host_chunk;
     if (host_chunk) {
-        for (int b = 0; b < 2; b++) {
+        for (int b = 0; b < dip_workspace::NBUF; b++) {
             CUDA_TRY(cudaMalloc(&w->d_rec[b], host_chunk * M->stride));
             CUDA_TRY(cudaEventCreateWithFlags(&w->ev_copied[b], cudaEventDisableTiming));
             CUDA_TRY(cudaEventCreateWithFlags(&w->ev_free[b], cudaEventDisableTiming));
         }
-        CUDA_TRY(cudaMalloc(&w->d_res, 2 * host_chunk * sizeof(dip_result)));
+        CUDA_TRY(cudaMalloc(&w->d_res, dip_workspace::NBUF * host_chunk * sizeof(dip_result)));
         CUDA_TRY(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&w->comp2, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&w->ev_start, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
+        CUDA_TRY(cudaMalloc(&w->d_spill2, w->spill_bytes));
     }
     *out = guard.release();
     return DIP_OK;
@@ -397,13 +401,17 @@ dip_status dip_workspace_free(dip_workspace *w) {
     if (w->d_misc) cudaFree(w->d_misc);
     if (w->h_misc) cudaFreeHost(w->h_misc);
     if (w->d_spill) cudaFree(w->d_spill);
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < dip_workspace::NBUF; b++) {
         if (w->d_rec[b]) cudaFree(w->d_rec[b]);
         if (w->ev_copied[b]) cudaEventDestroy(w->ev_copied[b]);
         if (w->ev_free[b]) cudaEventDestroy(w->ev_free[b]);
     }
     if (w->d_res) cudaFree(w->d_res);
     if (w->copy_stream) cudaStreamDestroy(w->copy_stream);
+    if (w->comp2) cudaStreamDestroy(w->comp2);
+    if (w->ev_start) cudaEventDestroy(w->ev_start);
+    if (w->ev_join) cudaEventDestroy(w->ev_join);
+    if (w->d_spill2) cudaFree(w->d_spill2);
     delete w;
     return DIP_OK;
 }
@@ -412,7 +420,8 @@ dip_status dip_workspace_free(dip_workspace *w) {
 extern "C++" {
 dip_status diph::launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                                uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
-                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out, const uint8_t *sel) {
+                               uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out, const uint8_t *sel,
+                               unsigned long long *spill, unsigned long long *counter) {
     KParams kp = M->kp;
     kp.records = static_cast<const uint8_t *>(d_records);
     kp.records_out = records_out;
@@ -423,12 +432,12 @@ dip_status diph::launch_chunk(const dip_model *M, dip_workspace *w, const void *
     kp.index_base = index_base;
     kp.results = d_results;
     kp.peaks = d_peaks;
-    kp.counter = w->d_misc + 0;
+    kp.counter = counter ? counter : w->d_misc + 0;
     kp.best_key = w->d_misc + 1;
-    kp.spill = w->d_spill;
+    kp.spill = spill ? spill : w->d_spill;
     kp.fused_key = fused ? 1u : 0u;
     kp.idx_bits = idx_bits;
-    CUDA_TRY(cudaMemsetAsync(w->d_misc + 0, 0, sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(kp.counter, 0, sizeof(unsigned long long), s));
     const int grid = (int)std::min<uint64_t>((uint64_t)M->grid,
                                              std::max<uint64_t>(1, (count + M->cpg * M->wpb - 1) / (M->cpg * M->wpb)));
     CUDA_TRY(dipk::launch_eval(kp, M->G, grid, M->wpb * 32, M->smem, s));
@@ -632,20 +641,27 @@ dip_status dip_eval_host(const dip_model *M, dip_workspace *w, const void *h_rec
     CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
     const size_t C = w->host_chunk;
     const size_t nch = (count + C - 1) / C;
+    CUDA_TRY(cudaEventRecord(w->ev_start, s));              // comp2 starts after the key reset
+    CUDA_TRY(cudaStreamWaitEvent(w->comp2, w->ev_start, 0));
     for (size_t c = 0; c < nch; c++) {
-        const int b = (int)(c & 1);
+        const int b = (int)(c % dip_workspace::NBUF);
+        const bool odd = (c & 1) != 0;
+        cudaStream_t sc = odd ? w->comp2 : s;
         const size_t lo = c * C, cnt = std::min(C, count - lo);
-        if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(w->copy_stream, w->ev_free[b], 0));
+        if (c >= (size_t)dip_workspace::NBUF) CUDA_TRY(cudaStreamWaitEvent(w->copy_stream, w->ev_free[b], 0));
         CUDA_TRY(cudaMemcpyAsync(w->d_rec[b], static_cast<const uint8_t *>(h_records) + lo * M->stride,
                                  cnt * M->stride, cudaMemcpyHostToDevice, w->copy_stream));
         CUDA_TRY(cudaEventRecord(w->ev_copied[b], w->copy_stream));
-        CUDA_TRY(cudaStreamWaitEvent(s, w->ev_copied[b], 0));
+        CUDA_TRY(cudaStreamWaitEvent(sc, w->ev_copied[b], 0));
         dip_result *dres = w->d_res + b * C;
-        dip_status st = launch_chunk(M, w, w->d_rec[b], cnt, lo, idx_bits, true, dres, nullptr, s);
+        dip_status st = launch_chunk(M, w, w->d_rec[b], cnt, lo, idx_bits, true, dres, nullptr, sc, nullptr, nullptr,
+                                     odd ? w->d_spill2 : w->d_spill, w->d_misc + (odd ? 8 : 0));
         if (st != DIP_OK) return st;
-        if (h_results) CUDA_TRY(cudaMemcpyAsync(h_results + lo, dres, cnt * sizeof(dip_result), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaEventRecord(w->ev_free[b], s));
+        if (h_results) CUDA_TRY(cudaMemcpyAsync(h_results + lo, dres, cnt * sizeof(dip_result), cudaMemcpyDeviceToHost, sc));
+        CUDA_TRY(cudaEventRecord(w->ev_free[b], sc));
     }
+    CUDA_TRY(cudaEventRecord(w->ev_join, w->comp2));        // the argmin sees both streams' chunks
+    CUDA_TRY(cudaStreamWaitEvent(s, w->ev_join, 0));
     w->last_results = nullptr;
     w->last_count = count;
     w->last_idx_bits = idx_bits;

@@ -69,7 +69,7 @@ struct dip_model {
 
 struct dip_workspace {
     const dip_model *model = nullptr;
-    unsigned long long *d_misc = nullptr;   // [0] counter [1] key [2] gkey [3] mk [4] idx [5..] spare
+    unsigned long long *d_misc = nullptr;   // [0] counter [1] key [2] gkey [3] mk [4] idx [5] f3 counter / fallback [6] fallback [8] comp2 counter
     unsigned long long *h_misc = nullptr;   // pinned
     unsigned long long *d_spill = nullptr;
     size_t spill_bytes = 0;
@@ -80,10 +80,16 @@ struct dip_workspace {
     bool last_fused = true;
     // host path
     size_t host_chunk = 0;
-    uint8_t *d_rec[2] = {nullptr, nullptr};
-    dip_result *d_res = nullptr;           // 2 * host_chunk results
-    cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    // host path: 3 staging buffers, copies on copy_stream, chunks alternating between the caller's
+    // stream and comp2 (each with its own spill area and work counter) so that one chunk's tail
+    // overlaps the next chunk's start
+    static constexpr int NBUF = 3;
+    uint8_t *d_rec[NBUF] = {nullptr, nullptr, nullptr};
+    dip_result *d_res = nullptr;           // NBUF * host_chunk results
+    cudaStream_t copy_stream = nullptr, comp2 = nullptr;
+    cudaEvent_t ev_copied[NBUF] = {nullptr, nullptr, nullptr}, ev_free[NBUF] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_join = nullptr;
+    unsigned long long *d_spill2 = nullptr;
 };
 
 struct dip_comm {
@@ -95,6 +101,7 @@ namespace diph {
 dip_status launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                         uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
                         uint32_t *d_peaks, cudaStream_t s, uint8_t *records_out = nullptr,
-                        const uint8_t *sel = nullptr);
+                        const uint8_t *sel = nullptr, unsigned long long *spill = nullptr,
+                        unsigned long long *counter = nullptr);
 bool fused_ok(const dip_model *M, uint32_t idx_bits);
 }  // namespace diph

@@ -66,12 +66,19 @@ __device__ __forceinline__ uint64_t group_max(uint64_t v) {
 }
 template <int G>
 __device__ __forceinline__ uint64_t group_min(uint64_t v) {
+    if constexpr (G == 32) {   // whole warp: two 32-bit REDUX (high word, then low word among its minima)
+        const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+        const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+        const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+        return ((uint64_t)mh << 32) | ml;
+    } else {
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o, G);
-        v = w < v ? w : v;
+        for (int o = G / 2; o > 0; o >>= 1) {
+            uint64_t w = __shfl_xor_sync(0xffffffffu, v, o, G);
+            v = w < v ? w : v;
+        }
+        return v;
     }
-    return v;
 }
 template <int G>
 __device__ __forceinline__ uint64_t group_sum(uint64_t v) {
@@ -472,28 +479,38 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
         const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
         const uint32_t bud = budget[laneOn ? r : 0];
+        // each lane's two queue heads are cached and re-evaluated only when a placement can change
+        // them: the placer's head in the placed direction, its consumer neighbour's head in that
+        // direction, and the wrap consumers (rank 0's F head after rank P-1 places an F, rank P-1's
+        // B head after rank 0 places a B or after rank P-1 places an F -- the loss turnaround)
+        uint2 eF = make_uint2(0u, 0u), eB = make_uint2(0u, 0u);
+        uint4 TF = make_uint4(0u, 0u, 0u, 0u), TB = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t layF = 0, layB = 0;
+        uint64_t tF = 0, tB = 0;
+        bool rdyF = false, rdyB = false, needF = true, needB = true;
         for (;;) {
             const uint32_t fu = __shfl_up_sync(FULL, fi, 1, G), bu = __shfl_up_sync(FULL, bi, 1, G);
             const uint32_t fd = __shfl_down_sync(FULL, fi, 1, G), bd = __shfl_down_sync(FULL, bi, 1, G);
-            const bool hasF = !done && fi < n, hasB = !done && bi < n;
-            // forward head
-            const uint2 eF = hasF ? posAll[fi] : make_uint2(0u, 0u);
-            const uint4 TF = tab[eF.x & 0xFFFu];
-            const uint32_t layF = layers[((eF.x >> 12) & 0xFFFu) + r];
-            const uint32_t nbF = fu;
-            uint64_t vF = hasF ? (isFirst ? depAll[eF.y & 0xFFFFu] : ringAll[(fi & (D - 1)) * P + colIn0]) : 0ull;
-            const bool rdyF = hasF && (isFirst ? (uint32_t)(vF >> 32) < (1u << 24) : nbF > fi);
-            if (rdyF && !isFirst && fi + D < nbF) vF = spill_load(spill, 0, r, P, n_max, fi);
-            const uint64_t tF = vF + (isFirst ? 0u : TF.w);   // used only when ready (pending byte 0)
-            // backward head
-            const uint2 eB = hasB ? posAll[n_max + bi] : make_uint2(0u, 0u);
-            const uint4 TB = tab[eB.x & 0xFFFu];
-            const uint32_t layB = layers[((eB.x >> 12) & 0xFFFu) + r];
-            const uint32_t nbB = bd;
-            uint64_t vB = hasB ? (isLast ? depAll[eB.y & 0xFFFFu] : ringAll[(bi & (D - 1)) * P + colIn1]) : 0ull;
-            const bool rdyB = hasB && (isLast ? (uint32_t)(vB >> 32) < (1u << 24) : nbB > bi);
-            if (rdyB && !isLast && bi + D < nbB) vB = spill_load(spill, 1, r, P, n_max, bi);
-            const uint64_t tB = vB + TB.w;
+            if (__any_sync(FULL, needF) && needF) {        // forward head
+                const bool hasF = !done && fi < n;
+                eF = hasF ? posAll[fi] : make_uint2(0u, 0u);
+                TF = tab[eF.x & 0xFFFu];
+                layF = layers[((eF.x >> 12) & 0xFFFu) + r];
+                uint64_t vF = hasF ? (isFirst ? depAll[eF.y & 0xFFFFu] : ringAll[(fi & (D - 1)) * P + colIn0]) : 0ull;
+                rdyF = hasF && (isFirst ? (uint32_t)(vF >> 32) < (1u << 24) : fu > fi);
+                if (rdyF && !isFirst && fi + D < fu) vF = spill_load(spill, 0, r, P, n_max, fi);
+                tF = vF + (isFirst ? 0u : TF.w);           // used only when ready (pending byte 0)
+            }
+            if (__any_sync(FULL, needB) && needB) {        // backward head
+                const bool hasB = !done && bi < n;
+                eB = hasB ? posAll[n_max + bi] : make_uint2(0u, 0u);
+                TB = tab[eB.x & 0xFFFu];
+                layB = layers[((eB.x >> 12) & 0xFFFu) + r];
+                uint64_t vB = hasB ? (isLast ? depAll[eB.y & 0xFFFFu] : ringAll[(bi & (D - 1)) * P + colIn1]) : 0ull;
+                rdyB = hasB && (isLast ? (uint32_t)(vB >> 32) < (1u << 24) : bd > bi);
+                if (rdyB && !isLast && bi + D < bd) vB = spill_load(spill, 1, r, P, n_max, bi);
+                tB = vB + TB.w;
+            }
             // memory gate and the group's argmin of (t_min, rank)
             const uint32_t actF = layF * TF.z;
             const bool gated = rdyF && cur + actF > bud;
@@ -515,6 +532,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 done = true;
             }
             __syncwarp();
+            uint32_t pdir = 0;
             if (!done && gk != INF && (uint32_t)(gk & 31u) == (uint32_t)r) {
                 const bool fOK = rdyF && (!gated || relax);
                 const bool bOK = rdyB;
@@ -563,6 +581,18 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 if (dir) bi++; else fi++;
                 last = (int)dir;
                 done = t + 1 == S2;
+                pdir = dir;
+            }
+            // which cached heads the group's placement (if any) may have changed
+            const uint32_t pl = (uint32_t)(gk & 31u);
+            const uint32_t dirw = __shfl_sync(FULL, pdir, (int)(pl & (G - 1)), G);
+            const bool placed = gk != INF;
+            needF = placed && dirw == 0 && ((uint32_t)r == pl || (uint32_t)r == pl + 1 || (isFirst && pl == P - 1));
+            needB = placed && ((dirw == 1 && ((uint32_t)r == pl || (uint32_t)r + 1 == pl || (isLast && pl == 0))) ||
+                               (dirw == 0 && isLast && pl == P - 1));
+            if constexpr (G < 32) {   // several groups per warp need both heads most steps: skip the test
+                needF = true;
+                needB = true;
             }
             __syncwarp();
         }
