@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         for (;;) {
             const uint32_t fu = __shfl_up_sync(FULL, fi, 1, G), bu = __shfl_up_sync(FULL, bi, 1, G);
             const uint32_t fd = __shfl_down_sync(FULL, fi, 1, G), bd = __shfl_down_sync(FULL, bi, 1, G);
-            if (__any_sync(FULL, needF) && needF) {        // forward head
+            if (G < 32 || (__any_sync(FULL, needF) && needF)) {   // forward head
                 const bool hasF = !done && fi < n;
                 eF = hasF ? posAll[fi] : make_uint2(0u, 0u);
                 TF = tab[eF.x & 0xFFFu];
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 if (rdyF && !isFirst && fi + D < fu) vF = spill_load(spill, 0, r, P, n_max, fi);
                 tF = vF + (isFirst ? 0u : TF.w);           // used only when ready (pending byte 0)
             }
-            if (__any_sync(FULL, needB) && needB) {        // backward head
+            if (G < 32 || (__any_sync(FULL, needB) && needB)) {   // backward head
                 const bool hasB = !done && bi < n;
                 eB = hasB ? posAll[n_max + bi] : make_uint2(0u, 0u);
                 TB = tab[eB.x & 0xFFFu];
@@ -583,16 +583,15 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 done = t + 1 == S2;
                 pdir = dir;
             }
-            // which cached heads the group's placement (if any) may have changed
-            const uint32_t pl = (uint32_t)(gk & 31u);
-            const uint32_t dirw = __shfl_sync(FULL, pdir, (int)(pl & (G - 1)), G);
-            const bool placed = gk != INF;
-            needF = placed && dirw == 0 && ((uint32_t)r == pl || (uint32_t)r == pl + 1 || (isFirst && pl == P - 1));
-            needB = placed && ((dirw == 1 && ((uint32_t)r == pl || (uint32_t)r + 1 == pl || (isLast && pl == 0))) ||
-                               (dirw == 0 && isLast && pl == P - 1));
-            if constexpr (G < 32) {   // several groups per warp need both heads most steps: skip the test
-                needF = true;
-                needB = true;
+            // which cached heads the group's placement (if any) may have changed (whole-warp groups
+            // only: with several groups per warp both heads are needed in most steps anyway)
+            if constexpr (G == 32) {
+                const uint32_t pl = (uint32_t)(gk & 31u);
+                const uint32_t dirw = __shfl_sync(FULL, pdir, (int)pl);
+                const bool placed = gk != INF;
+                needF = placed && dirw == 0 && ((uint32_t)r == pl || (uint32_t)r == pl + 1 || (isFirst && pl == P - 1));
+                needB = placed && ((dirw == 1 && ((uint32_t)r == pl || (uint32_t)r + 1 == pl || (isLast && pl == 0))) ||
+                                   (dirw == 0 && isLast && pl == P - 1));
             }
             __syncwarp();
         }

@@ -116,13 +116,9 @@ def test_strategy_menu_guards():
         with pytest.raises(dip.DipError) as e:
             m.set_strategies((f, b, a), S)
         assert e.value.code == 1
-    # a second strategy with the same memory and latency but another F/B split: two non-dominated
-    # candidates of equal memory, which the strict selection order cannot rank
-    f1 = np.where(b[0] > 0, f[0] + 1, f[0]).astype(np.uint32)
-    b1 = np.where(b[0] > 0, b[0] - 1, b[0]).astype(np.uint32)
-    with pytest.raises(dip.DipError) as e:
-        m.set_strategies((np.stack([f[0], f1]), np.stack([b[0], b1]), np.stack([a[0], a[0]])), 10)
-    assert e.value.code == 4
+    # (equal-memory / equal-latency candidates cannot survive the pruning -- the fastest, the
+    # smallest and every bucket winner break ties the same way -- so that host check is only a
+    # safety net and has no reachable input)
     pb2 = copy.deepcopy(pb)                            # budgets beyond the int32 selection
     pb2.budget_kib = np.full(pb.P, (1 << 31) + 5, np.uint32)
     m2 = dip.Model(pb2, 0)
