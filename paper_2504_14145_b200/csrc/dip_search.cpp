@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <thread>
@@ -39,6 +40,19 @@ inline uint64_t mix64(uint64_t x) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
+
+template <typename T>
+struct PinnedBuf {   // page-locked host array (falls back to pageable memory if pinning fails)
+    T *p = nullptr;
+    bool pinned = false;
+    explicit PinnedBuf(size_t n) {
+        if (cudaMallocHost(reinterpret_cast<void **>(&p), n * sizeof(T)) == cudaSuccess) pinned = true;
+        else p = static_cast<T *>(std::malloc(n * sizeof(T)));
+    }
+    ~PinnedBuf() { if (pinned) cudaFreeHost(p); else std::free(p); }
+    T &operator[](size_t i) { return p[i]; }
+    T *data() { return p; }
+};
 
 struct Node {
     int parent = -1;
@@ -183,8 +197,8 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     }
     const uint32_t R = prm->rollouts, B = prm->leaves;
     const size_t cap = (size_t)B * R;
-    std::vector<uint8_t> h_rec(cap * Md->stride);
-    std::vector<dip_result> h_res(cap);
+    PinnedBuf<uint8_t> h_rec(cap * Md->stride);      // pinned: the per-round H2D runs at full PCIe rate
+    PinnedBuf<dip_result> h_res(cap);
     uint8_t *d_rec = nullptr;
     dip_result *d_res = nullptr;
     uint8_t *d_sel = nullptr;
@@ -204,7 +218,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     for (; rd < prm->rounds; rd++) {
         // ---- selection + expansion of B leaves (virtual visits keep the batch diverse)
         std::vector<int> leaf(B);
-        std::vector<std::vector<uint32_t>> seqs;
+        std::vector<std::vector<uint32_t>> prefixes(B);
         std::vector<int> owner;
         std::vector<uint64_t> ctr;
         for (uint32_t l = 0; l < B; l++) {
@@ -243,32 +257,21 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
             }
             for (int x = v; x >= 0; x = tree[x].parent) tree[x].vloss++;
             leaf[l] = v;
-            // the fixed prefix, then R uniformly random completions (one for a complete sequence)
+            // the fixed prefix; its R uniformly random completions (one for a complete sequence) are
+            // drawn by the record-building threads below, each from its own counter-based stream
             std::vector<uint32_t> prefix;
             for (int x = v; x > 0; x = tree[x].parent) prefix.push_back((uint32_t)tree[x].cls);
             std::reverse(prefix.begin(), prefix.end());
-            std::vector<char> inpre(S.Cn, 0);
-            for (uint32_t c : prefix) inpre[c] = 1;
+            prefixes[l] = prefix;
             const uint32_t trials = (uint32_t)tree[v].depth == S.Cn ? 1 : R;
             for (uint32_t tr = 0; tr < trials; tr++) {
-                std::vector<uint32_t> rest;
-                for (uint32_t c = 0; c < S.Cn; c++) if (!inpre[c]) rest.push_back(c);
-                uint64_t rs = mix64(prm->seed ^ mix64(u + 0x51A9u));
-                for (uint32_t x = (uint32_t)rest.size(); x > 1; x--) {
-                    rs += 0x9E3779B97F4A7C15ull;
-                    const uint32_t y = (uint32_t)(mix64(rs) % x);
-                    std::swap(rest[x - 1], rest[y]);
-                }
-                std::vector<uint32_t> seq = prefix;
-                seq.insert(seq.end(), rest.begin(), rest.end());
-                seqs.push_back(seq);
                 owner.push_back((int)l);
                 ctr.push_back(u);
                 u++;
             }
         }
-        // ---- rollouts: build records on the host (threads), interleave + score on the GPU
-        const size_t cnt = seqs.size();
+        // ---- rollouts: sequences + records on the host (threads), interleave + score on the GPU
+        const size_t cnt = owner.size();
         {
             std::vector<std::thread> th;
             const size_t per = (cnt + nth - 1) / nth;
@@ -276,7 +279,24 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
                 const size_t lo = per * t, hi = std::min(cnt, lo + per);
                 if (lo >= hi) break;
                 th.emplace_back([&, lo, hi]() {
-                    for (size_t x = lo; x < hi; x++) build_record(Md, S, seqs[x], &h_rec[x * Md->stride]);
+                    std::vector<char> inpre(S.Cn);
+                    std::vector<uint32_t> seq, rest;
+                    for (size_t x = lo; x < hi; x++) {
+                        const std::vector<uint32_t> &prefix = prefixes[owner[x]];
+                        std::fill(inpre.begin(), inpre.end(), 0);
+                        for (uint32_t c : prefix) inpre[c] = 1;
+                        rest.clear();
+                        for (uint32_t c = 0; c < S.Cn; c++) if (!inpre[c]) rest.push_back(c);
+                        uint64_t rs = mix64(prm->seed ^ mix64(ctr[x] + 0x51A9u));
+                        for (uint32_t y = (uint32_t)rest.size(); y > 1; y--) {
+                            rs += 0x9E3779B97F4A7C15ull;
+                            const uint32_t z = (uint32_t)(mix64(rs) % y);
+                            std::swap(rest[y - 1], rest[z]);
+                        }
+                        seq.assign(prefix.begin(), prefix.end());
+                        seq.insert(seq.end(), rest.begin(), rest.end());
+                        build_record(Md, S, seq, &h_rec[x * Md->stride]);
+                    }
                 });
             }
             for (auto &t : th) t.join();

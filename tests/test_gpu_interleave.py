@@ -92,3 +92,18 @@ def test_interleave_deadlock_and_bad():
     c.fwd[1, 1] = c.fwd[1, 0]      # duplicate id -> BAD_ENCODING
     res = check(pb, c)
     assert res["status"].tolist() == [oracle.ST_DEADLOCK, oracle.ST_BAD]
+
+
+def test_interleave_bench_size_sampled():
+    # the bench's f1 launch shape: 65,536 94B candidates in one dip_interleave call; 10 of them
+    # (spread over the launch, incl. both ends) rebuilt by the oracle's interleaving
+    pb = gen.make_problem("94B")
+    cs = gen.generate(pb, 0, 65536, threads=16)
+    res, pk, bits, win, res2, pk2 = run_interleave(pb, cs)
+    idx = [0, 1, 4095, 4096, 20000, 32767, 32768, 50001, 65534, 65535]
+    rbits, ref = oracle.interleave(pb, cs.subset(idx), threads=16)
+    assert np.array_equal(bits[idx], rbits)
+    assert np.array_equal(res["status"][idx], ref.status)
+    assert np.array_equal(res["makespan_ns"][idx], ref.makespan)
+    assert np.array_equal(res["bubble"][idx].view(np.uint64), ref.bubble.view(np.uint64))
+    assert np.array_equal(pk[idx].astype(np.uint64), ref.peaks)
