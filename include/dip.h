@@ -263,7 +263,7 @@ dip_status dip_pack_key(uint64_t makespan_ns, uint32_t rank, uint64_t local, uin
 dip_status dip_unpack_key(uint64_t key, uint64_t shard_stride, uint32_t world, dip_winner *out);
 
 /* End to end from HOST records (pinned for overlap): chunked H2D copies overlapped
- * with scoring, then dip_argmin. h_results ([count], host) may be NULL. Requires a
+ * with scoring (chunks of min(host_chunk, max(8192, count/8)) records), then dip_argmin. h_results ([count], host) may be NULL. Requires a
  * workspace created with host_chunk > 0. Synchronous. */
 dip_status dip_eval_host(const dip_model *m, dip_workspace *w, const void *h_records, size_t count,
                          dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world,

@@ -639,7 +639,8 @@ dip_status dip_eval_host(const dip_model *M, dip_workspace *w, const void *h_rec
     const bool fused = fused_ok(M, idx_bits);
     if (!fused) return fail(DIP_ERANGE, "host path needs the fused argmin key (makespan bound too large)");
     CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
-    const size_t C = w->host_chunk;
+    // at least ~8 chunks when the batch allows it, so that the first copy (not overlapped) is short
+    const size_t C = std::min<size_t>(w->host_chunk, std::max<size_t>(8192, (count + 7) / 8));
     const size_t nch = (count + C - 1) / C;
     CUDA_TRY(cudaEventRecord(w->ev_start, s));              // comp2 starts after the key reset
     CUDA_TRY(cudaStreamWaitEvent(w->comp2, w->ev_start, 0));
