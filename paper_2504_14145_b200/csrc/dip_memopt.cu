@@ -159,12 +159,13 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
 
     uint8_t *wa = smem + (size_t)warp * warp_bytes;
     int32_t *slack = reinterpret_cast<int32_t *>(wa);                      // [n_max] (|values| < 2^31: host guard)
-    uint2 *dd = reinterpret_cast<uint2 *>(wa + 4 * ((n_max + 1) & ~1u));  // [n_max] next step (saving, KiB)
-    uint16_t *fw = reinterpret_cast<uint16_t *>(dd);                        // decode scratch, dead before dd is
+    uint32_t *key = reinterpret_cast<uint32_t *>(wa + 4 * ((n_max + 1) & ~1u));  // [n_max] next step's key
+    uint32_t *dms = key + n_max;                                            // [n_max] next step's KiB
+    uint16_t *fw = reinterpret_cast<uint16_t *>(key);                       // decode scratch, dead before key is
     uint16_t *invB = fw + n_max;                                            //   written: forward sequence,
     uint16_t *bsl = invB + n_max;                                           //   segment -> backward position,
                                                                             //   slot of the q-th backward
-    int32_t *cb = reinterpret_cast<int32_t *>(dd + n_max);                  // [n_max] ctab row of pair p
+    int32_t *cb = reinterpret_cast<int32_t *>(dms + n_max);                 // [n_max] ctab row of pair p
     uint16_t *eP = reinterpret_cast<uint16_t *>(cb + n_max);                // end of pair p's point range
     uint16_t *qp = eP + n_max;                                              // backward position of pair p
     uint8_t *cur = reinterpret_cast<uint8_t *>(qp + n_max);                 // selected candidate
@@ -304,28 +305,31 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             // largest ratio, ties to the lower p -- in one REDUX instead of a cross-multiplied
             // shuffle tournament
             for (uint32_t p = lane; p < n; p += 32) {
-                uint32_t key = 0, dm = 0;
+                uint32_t k = 0, dm = 0;
                 if (ncand[p] > 1) {
-                    key = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[p]])) << 16) | (0xFFFFu - p);
+                    k = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[p]])) << 16) | (0xFFFFu - p);
                     dm = __ldg(&kp.ctab[cb[p] + 1]).z - __ldg(&kp.ctab[cb[p]]).z;
                 }
-                dd[p] = make_uint2(key, dm);
+                key[p] = k;
+                dms[p] = dm;
             }
             __syncwarp();
             for (;;) {
                 // the best pair not yet known to be blocked; its feasibility is checked only now
                 // (lazily): a pair whose step does not fit is blocked for good (the slack never grows)
-                uint32_t best = 0;
-                for (uint32_t p = lane; p < n; p += 32) best = max(best, dd[p].x);
-                best = __reduce_max_sync(FULL, best);
+                uint32_t b0 = 0, b1 = 0;                   // two independent chains (ILP)
+                uint32_t p = lane;
+                for (; p + 32 < n; p += 64) { b0 = max(b0, key[p]); b1 = max(b1, key[p + 32]); }
+                if (p < n) b0 = max(b0, key[p]);
+                const uint32_t best = __reduce_max_sync(FULL, max(b0, b1));
                 if (best == 0) break;
-                const uint32_t a0 = 0xFFFFu - (best & 0xFFFFu), a1 = eP[a0], bdm = dd[a0].y;
+                const uint32_t a0 = 0xFFFFu - (best & 0xFFFFu), a1 = eP[a0], bdm = dms[a0];
                 int32_t mn = INF;
                 for (uint32_t k = a0 + lane; k < a1; k += 32) mn = min(mn, slack[k]);
                 mn = __reduce_min_sync(FULL, mn);
                 __syncwarp();
                 if ((int64_t)bdm > (int64_t)mn) {          // blocked for good
-                    if (lane == 0) dd[a0] = make_uint2(0u, 0u);
+                    if (lane == 0) key[a0] = 0;
                     __syncwarp();
                     continue;
                 }
@@ -333,12 +337,13 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 if (lane == 0) {
                     const uint32_t c = cur[a0] + 1u;
                     cur[a0] = (uint8_t)c;
-                    uint2 d = make_uint2(0u, 0u);
+                    uint32_t k = 0, dm = 0;
                     if (c + 1u < ncand[a0]) {
-                        d.x = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[a0] + c])) << 16) | (0xFFFFu - a0);
-                        d.y = __ldg(&kp.ctab[cb[a0] + c + 1]).z - __ldg(&kp.ctab[cb[a0] + c]).z;
+                        k = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[a0] + c])) << 16) | (0xFFFFu - a0);
+                        dm = __ldg(&kp.ctab[cb[a0] + c + 1]).z - __ldg(&kp.ctab[cb[a0] + c]).z;
                     }
-                    dd[a0] = d;
+                    key[a0] = k;
+                    dms[a0] = dm;
                 }
                 __syncwarp();
             }
