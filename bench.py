@@ -378,6 +378,13 @@ def main():
               "rollouts_per_s": sr["scored"] / dt, "rollouts": sr["scored"], "rounds": sr["rounds_done"],
               "wall_s": dt, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
               "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"]}
+        if world == 1 and not args.no_cpu_baseline:   # the oracle's search (single-threaded), 1 round x 64 leaves
+            import oracle
+            t0 = time.perf_counter()
+            orr = oracle.search(pb, cs.split[0], seed=pb.seed, rounds=1, leaves=64, rollouts=args.f2_rollouts)
+            dt = time.perf_counter() - t0
+            f2["cpu_oracle"] = {"value": orr["scored"] / dt, "unit": "rollouts/s", "cores": 1,
+                                "sample": f"1 round x 64 leaves x {args.f2_rollouts} rollouts ({dt:.1f} s)"}
 
     hbm_peak, sm_max, src = peaks()
     cpu = None

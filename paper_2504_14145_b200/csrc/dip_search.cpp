@@ -199,6 +199,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     const size_t cap = (size_t)B * R;
     PinnedBuf<uint8_t> h_rec(cap * Md->stride);      // pinned: the per-round H2D runs at full PCIe rate
     PinnedBuf<dip_result> h_res(cap);
+    if (!h_rec.data() || !h_res.data()) return fail(DIP_ENOMEM, "search host buffers");
     uint8_t *d_rec = nullptr;
     dip_result *d_res = nullptr;
     uint8_t *d_sel = nullptr;
