@@ -192,3 +192,53 @@ def test_host_end_to_end_path():
     assert np.array_equal(r["makespan_ns"], ref.makespan) and np.array_equal(r["status"], ref.status)
     best = oracle.argmin(ref.makespan, ref.status)
     assert win.found and win.global_index == best
+
+
+def test_maximum_shapes():
+    # the record format's extremes: P = 32 ranks and m = 255 microbatches (the u8 microbatch field),
+    # K = 4 chunks -> n = 1020 segments, 65,280 stage nodes per candidate: chunk-major forward order,
+    # reversed backward order; per-rank warm-ups n - 2r (then 1F1B), all-forward-first (GPipe), and
+    # one adjacent F/B swap -- bit-exact against the oracle
+    P, m, K = 32, 255, 4
+    n = m * K
+    pb = H.uniform_problem(P, m, 3, 5, act=2, p2p=1, K=K, budget=[4000] * P)
+    fseq = [b * K + k for k in range(K) for b in range(m)]
+    bseq = [b * K + k for k in reversed(range(K)) for b in range(m)]
+
+    def ranks(warm):
+        out = []
+        for r in range(P):
+            w = warm(r)
+            seq = [("F", s) for s in fseq[:w]]
+            f, b = w, 0
+            while b < n:
+                seq.append(("B", bseq[b]))
+                b += 1
+                if f < n:
+                    seq.append(("F", fseq[f]))
+                    f += 1
+            out.append(seq)
+        return out
+
+    orders = [ranks(lambda r: n - 2 * r), ranks(lambda r: n)]
+    cs = H.candidates_from_orders(pb, [[1] * m] * 2, orders)
+    cs2 = cs.subset([0, 1, 0])
+    fb = cs2.fb[2, 7].copy()
+    bits = [(int(fb[t >> 5]) >> (t & 31)) & 1 for t in range(2 * n)]
+    t = next(t for t in range(1000, 2 * n - 1) if bits[t] != bits[t + 1])
+    bits[t], bits[t + 1] = bits[t + 1], bits[t]
+    cs2.fb[2, 7] = 0
+    for i, bit in enumerate(bits):
+        if bit:
+            cs2.fb[2, 7, i >> 5] |= np.uint32(1 << (i & 31))
+    res, pk, win = run_gpu(pb, cs2)
+    assert_parity(pb, cs2, res, pk, win)
+    assert res["status"][0] in (oracle.ST_OK, oracle.ST_OOM) and res["status"][1] in (oracle.ST_OK, oracle.ST_OOM)
+
+
+def test_working_set_too_large_is_rejected():
+    # n_max = 255 * 64 segments: the per-candidate shared-memory working set cannot fit -> DIP_ERANGE
+    pb = H.uniform_problem(2, 255, 1, 2, K=64)
+    with pytest.raises(dip.DipError) as e:
+        dip.Model(pb, 0)
+    assert e.value.code == 4
