@@ -294,97 +294,106 @@ def main():
 
     # ---- DIP's dual-queue interleaving on the first f1-count records
     f1 = None
-    if args.f1_count > 0:
-        cnt = min(per, args.f1_count)
-        d_f1 = d_rec[: cnt * model.stride].clone()
-        r_f1 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
-        for _ in range(2):
-            dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = max(1, min(args.steps, 5))
-        a.record(stream)
-        for _ in range(reps):
-            dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        tf1 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tf1, op=dist.ReduceOp.MAX)
-        f1 = {"what": "dip_interleave: build each candidate's F/B interleaving with the paper's dual-queue "
-                      "greedy (P:511-548) from its split + priority orders, then score it",
-              "value": cnt * world * reps / (float(tf1[0]) / 1e3), "unit": "candidates/s",
-              "candidates_per_gpu": cnt, "ms_per_call": float(tf1[0]) / reps}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            import oracle
-            sub = cs.subset(np.arange(min(cnt, 2048)))
-            t0 = time.perf_counter()
-            oracle.interleave(pb, sub, threads=os.cpu_count() or 1)
-            f1["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
-                                "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
-        del d_f1, r_f1
+    try:
+        if args.f1_count > 0:
+            cnt = min(per, args.f1_count)
+            d_f1 = d_rec[: cnt * model.stride].clone()
+            r_f1 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
+            for _ in range(2):
+                dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, min(args.steps, 5))
+            a.record(stream)
+            for _ in range(reps):
+                dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tf1 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tf1, op=dist.ReduceOp.MAX)
+            f1 = {"what": "dip_interleave: build each candidate's F/B interleaving with the paper's dual-queue "
+                          "greedy (P:511-548) from its split + priority orders, then score it",
+                  "value": cnt * world * reps / (float(tf1[0]) / 1e3), "unit": "candidates/s",
+                  "candidates_per_gpu": cnt, "ms_per_call": float(tf1[0]) / reps}
+            if rank == 0 and world == 1 and not args.no_cpu_baseline:
+                import oracle
+                sub = cs.subset(np.arange(min(cnt, 2048)))
+                t0 = time.perf_counter()
+                oracle.interleave(pb, sub, threads=os.cpu_count() or 1)
+                f1["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
+                                    "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
+            del d_f1, r_f1
+    except Exception as ex:   # a side measurement must not cost the headline line
+        f1 = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     # ---- per-layer memory optimisation on the first f3-count records
     f3 = None
-    if args.f3_count > 0:
-        from gen.problem import strategy_menu
-        menu = strategy_menu(pb)
-        model.set_strategies(menu, 10)
-        cnt = min(per, args.f3_count)
-        d_sel = torch.empty(cnt * pb.P * 2 * pb.n_max, dtype=torch.uint8, device=dev)
-        r_f3 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
-        for _ in range(2):
-            dip.memopt(model, ws, d_rec, cnt, d_sel, r_f3, None, stream=stream)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = max(1, min(args.steps, 5))
-        a.record(stream)
-        for _ in range(reps):
-            dip.memopt(model, ws, d_rec, cnt, d_sel, r_f3, None, stream=stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        tf3 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tf3, op=dist.ReduceOp.MAX)
-        r3 = dip.results_view(r_f3.cpu().numpy())
-        base = dip.results_view(d_res[: cnt * 24].cpu().numpy())
-        ok = (r3["status"] == 0) & (base["status"] == 0)
-        gain = float(np.median(r3["makespan_ns"][ok] / base["makespan_ns"][ok])) if ok.any() else None
-        f3 = {"what": "dip_memopt: per-rank greedy strategy selection under the memory budget (P:569-590) "
-                      "over GPU-built knapsack candidates (P:558-567, S = 10, 3 strategies), then re-timing",
-              "value": cnt * world * reps / (float(tf3[0]) / 1e3), "unit": "candidates/s",
-              "candidates_per_gpu": cnt, "ms_per_call": float(tf3[0]) / reps,
-              "median_makespan_ratio_vs_base": gain}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            import oracle
-            sub = cs.subset(np.arange(min(cnt, 64)))
-            t0 = time.perf_counter()
-            oracle.memopt(pb, sub, menu, S=10, threads=os.cpu_count() or 1)
-            f3["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
-                                "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
-        del d_sel, r_f3
+    try:
+        if args.f3_count > 0:
+            from gen.problem import strategy_menu
+            menu = strategy_menu(pb)
+            model.set_strategies(menu, 10)
+            cnt = min(per, args.f3_count)
+            d_sel = torch.empty(cnt * pb.P * 2 * pb.n_max, dtype=torch.uint8, device=dev)
+            r_f3 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
+            for _ in range(2):
+                dip.memopt(model, ws, d_rec, cnt, d_sel, r_f3, None, stream=stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, min(args.steps, 5))
+            a.record(stream)
+            for _ in range(reps):
+                dip.memopt(model, ws, d_rec, cnt, d_sel, r_f3, None, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tf3 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tf3, op=dist.ReduceOp.MAX)
+            r3 = dip.results_view(r_f3.cpu().numpy())
+            base = dip.results_view(d_res[: cnt * 24].cpu().numpy())
+            ok = (r3["status"] == 0) & (base["status"] == 0)
+            gain = float(np.median(r3["makespan_ns"][ok] / base["makespan_ns"][ok])) if ok.any() else None
+            f3 = {"what": "dip_memopt: per-rank greedy strategy selection under the memory budget (P:569-590) "
+                          "over GPU-built knapsack candidates (P:558-567, S = 10, 3 strategies), then re-timing",
+                  "value": cnt * world * reps / (float(tf3[0]) / 1e3), "unit": "candidates/s",
+                  "candidates_per_gpu": cnt, "ms_per_call": float(tf3[0]) / reps,
+                  "median_makespan_ratio_vs_base": gain}
+            if rank == 0 and world == 1 and not args.no_cpu_baseline:
+                import oracle
+                sub = cs.subset(np.arange(min(cnt, 64)))
+                t0 = time.perf_counter()
+                oracle.memopt(pb, sub, menu, S=10, threads=os.cpu_count() or 1)
+                f3["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
+                                    "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
+            del d_sel, r_f3
+    except Exception as ex:   # a side measurement must not cost the headline line
+        f3 = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     # ---- MCTS segment reordering with batched GPU rollouts, for the
     # split of candidate 0 of this shard (rank 0 only; a search is one planner's job)
     f2 = None
-    if args.f2_rounds > 0 and rank == 0:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        sr = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,
-                        rollouts=args.f2_rollouts, alpha=1.0, beta=0.5, stream=stream)
-        dt = time.perf_counter() - t0
-        f2 = {"what": "dip_search: MCTS over class priorities (P:472-509), rollouts = priorities -> f1 interleaving "
-                      "-> score, one batched GPU launch per round",
-              "rollouts_per_s": sr["scored"] / dt, "rollouts": sr["scored"], "rounds": sr["rounds_done"],
-              "wall_s": dt, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
-              "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"]}
-        if world == 1 and not args.no_cpu_baseline:   # the oracle's search (single-threaded), 1 round x 64 leaves
-            import oracle
+    try:
+        if args.f2_rounds > 0 and rank == 0:
+            torch.cuda.synchronize()
             t0 = time.perf_counter()
-            orr = oracle.search(pb, cs.split[0], seed=pb.seed, rounds=1, leaves=64, rollouts=args.f2_rollouts)
+            sr = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,
+                            rollouts=args.f2_rollouts, alpha=1.0, beta=0.5, stream=stream)
             dt = time.perf_counter() - t0
-            f2["cpu_oracle"] = {"value": orr["scored"] / dt, "unit": "rollouts/s", "cores": 1,
-                                "sample": f"1 round x 64 leaves x {args.f2_rollouts} rollouts ({dt:.1f} s)"}
+            f2 = {"what": "dip_search: MCTS over class priorities (P:472-509), rollouts = priorities -> f1 interleaving "
+                          "-> score, one batched GPU launch per round",
+                  "rollouts_per_s": sr["scored"] / dt, "rollouts": sr["scored"], "rounds": sr["rounds_done"],
+                  "wall_s": dt, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
+                  "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"]}
+            if world == 1 and not args.no_cpu_baseline:   # the oracle's search (single-threaded), 1 round x 64 leaves
+                import oracle
+                t0 = time.perf_counter()
+                orr = oracle.search(pb, cs.split[0], seed=pb.seed, rounds=1, leaves=64, rollouts=args.f2_rollouts)
+                dt = time.perf_counter() - t0
+                f2["cpu_oracle"] = {"value": orr["scored"] / dt, "unit": "rollouts/s", "cores": 1,
+                                    "sample": f"1 round x 64 leaves x {args.f2_rollouts} rollouts ({dt:.1f} s)"}
+    except Exception as ex:   # a side measurement must not cost the headline line
+        f2 = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     hbm_peak, sm_max, src = peaks()
     cpu = None
