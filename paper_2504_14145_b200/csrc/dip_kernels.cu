@@ -16,6 +16,11 @@
 // RING_D) with an exact spill to global memory when a producer runs more than RING_D
 // stages ahead of its consumer, so the lock-step wavefront never blocks on a full channel
 // (no false deadlocks: "no lane can progress" <=> the candidate's DAG has a cycle).
+//
+// The same kernel template serves the §8(f) rows: MODE 1 builds each candidate's F/B
+// interleaving with DIP's dual-queue greedy first (f1), MODE 2 also records every
+// stage's start / end (f4's timelines), MODE 3 takes each stage pair's latency and activation
+// from the f3 candidate table through a per-(candidate, rank, position) selection.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -107,9 +112,6 @@ constexpr uint32_t E_MULTI = 4u << 24;    // several join targets: slower loop (
 //   slot = max(slot, (slot & HIGH) | value) + (1 << 56)
 constexpr uint64_t HIGH_MASK = ~VAL_MASK;
 
-#ifndef DIP_KP
-#define DIP_KP 0   // A/B: keep the current position's rows in registers across rounds
-#endif
 
 
 // rare paths kept out of line (a call is never if-converted into the round's common path)
@@ -362,35 +364,20 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
         const uint32_t wrapBits = (isFirst ? 1u : 0u) | (isLast ? 2u : 0u);   // bit d: consumes dir d via wrap
         const uint32_t wrapPub = (isLast ? 1u : 0u) | (isFirst ? 2u : 0u);    // bit d: publishes dir d via wrap
-#if DIP_KP
-        // the current position's row, cost row and layer count live in registers: they change only
-        // when the lane places its stage, and are then fetched for the next position at once, off
-        // the next round's dependency chain
-        uint32_t d = wcur & 1u;
-        uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max];
-        uint4 T = tab[e.x & 0xFFFu];
-        uint32_t lay = layers[((e.x >> 12) & 0xFFFu) + r];
-#endif
         for (;;) {
-#if !DIP_KP
             const uint32_t d = (wcur >> (t & 31)) & 1u;            // 0 = F, 1 = B
-#endif
             const bool wrapC = (wrapBits >> d) & 1u;
             const bool wrapP = (wrapPub >> d) & 1u;
             const uint32_t fu = __shfl_up_sync(FULL, cF, 1, G), bu = __shfl_up_sync(FULL, cB, 1, G);
             const uint32_t fd = __shfl_down_sync(FULL, cF, 1, G), bd = __shfl_down_sync(FULL, cB, 1, G);
             const uint32_t idx = d ? cB : cF;
             const uint32_t nb = wrapC ? 0xFFFFu : (d ? bd : fu);                        // producer's count
-#if !DIP_KP
             const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];       // done lanes: a safe row
-#endif
             const uint32_t ring = (idx & (D - 1)) * P;
             const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (d ? colIn1 : colIn0)];
             uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)] : &ringAll[ring + (d ? colOut1 : colOut0)];
-#if !DIP_KP
             const uint4 T = tab[e.x & 0xFFFu];
             const uint32_t lay = layers[((e.x >> 12) & 0xFFFu) + r];
-#endif
             const uint64_t v = *ca;
             const uint64_t pold = *pa;
             // a ready value has a zero pending byte, so it needs no mask (v < 2^56 <=> high word < 2^24)
@@ -460,12 +447,6 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                     wptr += P;
                 }
                 done = t == S2;
-#if DIP_KP
-                d = (wcur >> (t & 31)) & 1u;
-                e = done ? make_uint2(0u, 0u) : posAll[d * n_max + (d ? cB : cF)];
-                T = tab[e.x & 0xFFFu];
-                lay = layers[((e.x >> 12) & 0xFFFu) + r];
-#endif
             }
             __syncwarp();
         }
