@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -216,7 +218,11 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     int nth = prm->threads > 0 ? prm->threads : (int)std::max(1u, std::thread::hardware_concurrency());
     dip_status status = DIP_OK;
     uint32_t rd = 0;
+    const bool prof = std::getenv("DIP_SEARCH_PROFILE") != nullptr;   // per-phase wall times to stderr
+    double t_sel = 0, t_build = 0, t_gpu = 0, t_back = 0;
+    auto now = []() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     for (; rd < prm->rounds; rd++) {
+        double t0 = now();
         // ---- selection + expansion of B leaves (virtual visits keep the batch diverse)
         std::vector<int> leaf(B);
         std::vector<std::vector<uint32_t>> prefixes(B);
@@ -273,6 +279,8 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
         }
         // ---- rollouts: sequences + records on the host (threads), interleave + score on the GPU
         const size_t cnt = owner.size();
+        double t1 = now();
+        t_sel += t1 - t0;
         {
             std::vector<std::thread> th;
             const size_t per = (cnt + nth - 1) / nth;
@@ -302,6 +310,8 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
             }
             for (auto &t : th) t.join();
         }
+        double t2 = now();
+        t_build += t2 - t1;
         if (cudaMemcpyAsync(d_rec, h_rec.data(), cnt * Md->stride, cudaMemcpyHostToDevice, st) != cudaSuccess) {
             status = fail(DIP_ECUDA, "search H2D");
             break;
@@ -318,6 +328,8 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
             break;
         }
         scored += cnt;
+        double t3 = now();
+        t_gpu += t3 - t2;
         // ---- backpropagation, leaf by leaf
         std::vector<double> lbest(B, 0.0);
         size_t arg = cnt;
@@ -339,7 +351,11 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
             }
         }
         if (trace) trace[rd] = best;
+        t_back += now() - t3;
     }
+    if (prof)
+        std::fprintf(stderr, "dip_search: select %.1f ms, build %.1f ms, gpu %.1f ms, backprop %.1f ms over %u rounds\n",
+                     t_sel * 1e3, t_build * 1e3, t_gpu * 1e3, t_back * 1e3, rd);
     cudaFree(d_rec);
     cudaFree(d_res);
     if (d_sel) cudaFree(d_sel);
