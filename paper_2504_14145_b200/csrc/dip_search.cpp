@@ -250,13 +250,14 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
                     v = id;
                     break;
                 }
-                const double Nx = (double)(nd.N + nd.vloss);
+                const double Nx = (double)(nd.N + nd.vloss), lnNx = std::log(Nx);
+                const bool a1 = prm->alpha == 1.0;       // pow(s, 1) is s exactly: skip the call
                 int bestc = -1;
                 double bu = -1.0;
                 for (int c : nd.children) {
                     const Node &cn = tree[c];
                     const double Nv = (double)(cn.N + cn.vloss);
-                    const double ucb = std::pow(cn.s, prm->alpha) + prm->beta * std::sqrt(std::log(Nx) / Nv);
+                    const double ucb = (a1 ? cn.s : std::pow(cn.s, prm->alpha)) + prm->beta * std::sqrt(lnNx / Nv);
                     if (ucb > bu) { bu = ucb; bestc = c; }
                 }
                 used[tree[bestc].cls] = 1;
