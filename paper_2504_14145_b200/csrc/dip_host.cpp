@@ -66,7 +66,11 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     if (m < 1 || m > 255) return fail(DIP_EINVAL, "m must be in 1..255");
     dip_model *M = new (std::nothrow) dip_model();
     if (!M) return fail(DIP_ENOMEM, "host allocation");
-    std::unique_ptr<dip_model> guard(M);
+    struct Guard {   // on any failure below, release what was allocated so far
+        dip_model *m;
+        ~Guard() { if (m) dip_model_free(m); }
+        dip_model *release() { dip_model *x = m; m = nullptr; return x; }
+    } guard{M};
     M->device = cuda_device;
     M->P = P; M->nmod = nm; M->m = m;
 
@@ -370,7 +374,11 @@ dip_status dip_workspace_create(const dip_model *M, size_t host_chunk, dip_works
     CUDA_TRY(cudaSetDevice(M->device));
     dip_workspace *w = new (std::nothrow) dip_workspace();
     if (!w) return fail(DIP_ENOMEM, "host allocation");
-    std::unique_ptr<dip_workspace> guard(w);
+    struct Guard {   // on any failure below, release what was allocated so far
+        dip_workspace *w;
+        ~Guard() { if (w) dip_workspace_free(w); }
+        dip_workspace *release() { dip_workspace *x = w; w = nullptr; return x; }
+    } guard{w};
     w->model = M;
     CUDA_TRY(cudaMalloc(&w->d_misc, 16 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemset(w->d_misc, 0, 16 * sizeof(unsigned long long)));
