@@ -411,6 +411,17 @@ def main():
             with open(tp) as f:
                 tj = json.load(f)
             traffic = tj["dram_bytes_per_candidate"] * per
+        issue = None
+        fp = os.path.join(ROOT, "profiles", f"r01_ncu_full_{args.config}.json")
+        if os.path.exists(fp):   # warp instructions per candidate from the same capture: the issue ceiling
+            with open(fp) as f:
+                wi = json.load(f).get("warp_inst_per_candidate")
+            if wi:
+                ach = wi * per / kern_s
+                pk = 4 * 148 * sm_max * 1e6
+                issue = {"achieved": ach / 1e12, "peak": pk / 1e12, "unit": "T warp-instr/s", "frac": ach / pk,
+                         "source": f"profiles/r01_ncu_full_{args.config}.json ({wi:.0f} warp instructions per candidate)"
+                                   " x candidates / kernel time vs 4 issue slots/clk/SM x 148 SMs x sm_max"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -426,6 +437,7 @@ def main():
             "hbm": {"achieved": bytes_launch / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bytes_launch / kern_s / 1e9 / hbm_peak,
                     "algorithmic": "record + 24 B result + 4P B peaks per candidate", "peak_source": src},
+            "issue": issue,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks, "f1_interleave": f1, "f2_search": f2,
             "f3_memopt": f3,
             "status_hist": {"ok": hist[0], "oom": hist[1], "deadlock": hist[2], "bad_encoding": hist[3]},
