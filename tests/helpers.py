@@ -115,3 +115,30 @@ def vpp(P: int, v: int, m: int) -> List[List[Tuple[str, int]]]:
                 f += 1
         out.append(seq)
     return out
+
+
+def diamond_problem(P: int = 4, m: int = 6, seed: int = 0) -> Problem:
+    """Four modules in a diamond: vision (M_max 4) and audio (M_max 2) both feed a fusion module
+    (K = 2, M_max 2) that feeds an LLM (K = 2) -- joins with several producer modules and split
+    sub-microbatches on both sides, some microbatches without vision or audio instances."""
+    rng = np.random.default_rng(seed)
+    w = 8
+
+    def tab(scale):
+        return table(w, {u: (scale * u + 5, 2 * scale * u + 9, 3 * u, u) for u in range(1, w + 1)})
+
+    mods = [Module("vision", 2 * P, 1, 4, w, 0, *tab(7)),
+            Module("audio", P, 1, 2, w, 0, *tab(5)),
+            Module("fusion", 2 * P * 2, 2, 2, w, 0b011, *tab(3)),
+            Module("llm", 4 * P, 2, 1, w, 0b100, *tab(11))]
+    units, off = [], [0]
+    for b in range(m):
+        nv = int(rng.integers(0, 5)) if b % 3 else 0          # every third microbatch: no vision
+        na = int(rng.integers(0, 3))
+        per = [[int(rng.integers(1, 3)) for _ in range(nv)], [int(rng.integers(1, 5)) for _ in range(na)],
+               [int(rng.integers(1, 5)) for _ in range(int(rng.integers(1, 3)))], [int(rng.integers(1, 9))]]
+        for lst in per:
+            units += lst
+            off.append(len(units))
+    return Problem("diamond", P, m, mods, np.array(off, np.uint32), np.array(units, np.uint16),
+                   np.full(P, 700, np.uint32))

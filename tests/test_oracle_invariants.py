@@ -85,3 +85,15 @@ def test_generator_statuses_mostly_timed():
     timed = ((r.status == OK) | (r.status == OOM)).mean()
     assert timed >= 0.9
     assert (r.status == BAD).sum() == ((cs.family >> 6) & 1).sum() or (r.status == BAD).sum() > 0
+
+
+def test_diamond_modules_agree_with_independent_evaluator():
+    # four modules in a diamond (two producer modules joined by a K = 2 fusion module feeding a
+    # K = 2 LLM), split sub-microbatches on both sides of each join, microbatches without vision
+    from tests import helpers as H
+    pb = H.diamond_problem()
+    cs = gen.generate(pb, 0, 120, p_mutate=0.1, p_bad=0.05)
+    r = oracle.evaluate(pb, cs, threads=4)
+    _agree(pb, cs, r, range(120))
+    hist = np.bincount(r.status, minlength=4)
+    assert hist[OK] > 0 and hist[OOM] > 0 and hist[DL] > 0 and hist[BAD] > 0
