@@ -19,9 +19,10 @@ from tests import test_gpu_interleave as TI  # noqa: E402
 from tests import test_gpu_memopt as TM  # noqa: E402
 
 
-@pytest.fixture(scope="module")
-def diamond():
-    pb = H.diamond_problem()
+@pytest.fixture(scope="module", params=[3, 4, 6])
+def diamond(request):
+    # P = 3 and 6 leave idle lanes in the G = 4 / 8 lane groups
+    pb = H.diamond_problem(P=request.param)
     return pb, gen.generate(pb, 0, 512, p_mutate=0.1, p_bad=0.05)
 
 
