@@ -211,6 +211,9 @@ def main():
     ws = dip.Workspace(model, host_chunk=0 if args.no_e2e else args.host_chunk)
     h_rec = torch.empty(per * model.stride, dtype=torch.uint8).pin_memory()
     model.encode(cs, out=h_rec, threads=gthreads)
+    n_seg = cs.n.astype(np.int64)                     # per-candidate segment counts (stage-node totals)
+    if world > 1:   # the host-view arrays are only needed by rank 0's single-GPU side legs: free them
+        cs = cs.subset(np.arange(min(per, 64)))
     d_rec = h_rec.to(dev)
     d_res = torch.empty(per * 24, dtype=torch.uint8, device=dev)
     d_pk = torch.empty((per, pb.P), dtype=torch.int32, device=dev)
@@ -229,7 +232,7 @@ def main():
         win = step()
     res = dip.results_view(d_res.cpu().numpy())
     hist = np.bincount(res["status"], minlength=4).tolist()
-    stages = int(np.sum(np.where(res["status"] != 3, 2 * cs.n.astype(np.int64) * pb.P, 0)))
+    stages = int(np.sum(np.where(res["status"] != 3, 2 * n_seg * pb.P, 0)))
 
     # ---- timed region: device-resident inputs
     if world > 1:
