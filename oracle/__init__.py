@@ -176,9 +176,10 @@ def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha:
     fwd = np.zeros(pb.n_max, np.uint16)
     bwd = np.zeros(pb.n_max, np.uint16)
     bits = np.zeros((pb.P, pb.fbw), np.uint32)
+    arrs = _menu_arrays(menu)                     # kept alive for the call
     lib.oracle_search(ctypes.byref(bd.pb), pb.n_max, pb.fbw, sp.ctypes.data, seed & ((1 << 64) - 1), rounds, leaves,
                       rollouts, alpha, beta, trace.ctypes.data, ctypes.byref(sc), ctypes.byref(mk), fwd.ctypes.data,
-                      bwd.ctypes.data, bits.ctypes.data, ctypes.byref(scored), *_menu_args(menu, S))
+                      bwd.ctypes.data, bits.ctypes.data, ctypes.byref(scored), *_menu_args(arrs, S))
     return dict(score=sc.value, makespan=mk.value, trace=trace, fwd=fwd, bwd=bwd, bits=bits, scored=scored.value)
 
 
@@ -195,11 +196,15 @@ def timeline(pb, cands, x: int):
     return status, st[:pb.P * 2 * n].reshape(pb.P, 2 * n), en[:pb.P * 2 * n].reshape(pb.P, 2 * n)
 
 
-def _menu_args(menu, S):
-    if menu is None:
+def _menu_arrays(menu):
+    """contiguous uint32 (f, b, act) of a strategy menu, or None"""
+    return None if menu is None else tuple(np.ascontiguousarray(v, np.uint32) for v in menu)
+
+
+def _menu_args(arrs, S):
+    if arrs is None:
         return (0, None, None, None, S)
-    f, b, a = (np.ascontiguousarray(v, np.uint32) for v in menu)
-    _menu_args.keep = (f, b, a)
+    f, b, a = arrs
     return (f.shape[0], f.ctypes.data, b.ctypes.data, a.ctypes.data, S)
 
 
