@@ -1,0 +1,10 @@
+set -x
+DIP_LIB=paper_2504_14145_b200/libdip_mp.so timeout 900 python -m pytest tests/test_gpu_interleave.py tests/test_gpu_search.py tests/test_gpu_diamond.py tests/test_gpu_pipeline.py -x -q > gpurun_out/ab_par_mp.log 2>&1; echo par mp rc=$?
+for rep in 1 2; do
+  for v in base mp; do
+    if [ $v = base ]; then L=paper_2504_14145_b200/libdip.so; else L=paper_2504_14145_b200/libdip_$v.so; fi
+    DIP_LIB=$L python bench.py --steps 2 --no-e2e --no-cpu-baseline --f3-count 0 > gpurun_out/ab3_${v}_$rep.log 2>&1; echo bench $v $rep rc=$?
+  done
+done
+DIP_LIB=paper_2504_14145_b200/libdip_mp.so python bench.py --config 12B --steps 2 --no-e2e --no-cpu-baseline --f3-count 0 > gpurun_out/ab3_mp_12B.log 2>&1
+python bench.py --config 12B --steps 2 --no-e2e --no-cpu-baseline --f3-count 0 > gpurun_out/ab3_base_12B.log 2>&1
