@@ -215,7 +215,9 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     tree.reserve(1 + (size_t)prm->rounds * B);
     double best = -1.0;
     uint64_t best_mk = ~0ull, u = 0, scored = 0;
+    // record-building threads: all cores by default, but not more than one per 32 rollouts of a round
     int nth = prm->threads > 0 ? prm->threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    nth = std::max(1, std::min<int>(nth, (int)((cap + 31) / 32)));
     dip_status status = DIP_OK;
     uint32_t rd = 0;
     const bool prof = std::getenv("DIP_SEARCH_PROFILE") != nullptr;   // per-phase wall times to stderr
