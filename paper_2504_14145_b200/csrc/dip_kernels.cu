@@ -560,25 +560,31 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 cur = dir ? cur - act : cur + act;
                 peak = cur > peak ? cur : peak;
                 const bool wrapP = dir ? isFirst : isLast;
-                uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)]
-                                     : &ringAll[(idx & (D - 1)) * P + (dir ? colOut1 : colOut0)];
-                const uint64_t pold = *pa;
-                const int32_t sgn = (int32_t)(e.x << 6) >> 30;
-                const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
-                const uint64_t cand2 = (pold & HIGH_MASK) | pv;
-                *pa = wrapP ? (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT) : end;
+                // one lane places, so the publication can branch freely: a plain channel write for
+                // interior ranks, the wrap-slot read-modify-write only at rank 0 / P-1
                 if (!wrapP) {
+                    uint64_t *pa = &ringAll[(idx & (D - 1)) * P + (dir ? colOut1 : colOut0)];
+                    const uint64_t pold = *pa;
+                    *pa = end;
                     const uint32_t ccnt = dir ? bu : fd;                     // consumer neighbour's count
                     if (idx >= ccnt + D) spill_keep(spill, dir, r, P, n_max, idx, pold);
-                } else if (e.x & E_MULTI) {
-                    const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
-                    const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
-                    const uint32_t msk = dir ? mi[i].prod_mask : mi[i].cons_mask;
-                    for (uint32_t c = 0; c < nmod; c++) {
-                        if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
-                        uint64_t *sl = &depAll[dir ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
-                        const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
-                        *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                } else {
+                    uint64_t *pa = &depAll[min(e.y >> 16, SINK)];
+                    const uint64_t pold = *pa;
+                    const int32_t sgn = (int32_t)(e.x << 6) >> 30;
+                    const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
+                    const uint64_t cand2 = (pold & HIGH_MASK) | pv;
+                    *pa = (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT);
+                    if (e.x & E_MULTI) {
+                        const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
+                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
+                        const uint32_t msk = dir ? mi[i].prod_mask : mi[i].cons_mask;
+                        for (uint32_t c = 0; c < nmod; c++) {
+                            if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                            uint64_t *sl = &depAll[dir ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
+                            const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
+                            *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                        }
                     }
                 }
                 const uint32_t t = fi + bi;
