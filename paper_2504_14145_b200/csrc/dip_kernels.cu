@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "dip_internal.h"
 
 namespace dipk {
@@ -547,46 +549,53 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 else if (!fOK) dir = 1u;
                 else if (!bOK) dir = 0u;
                 else dir = tB <= tF ? 1u : 0u;
-                const uint2 e = dir ? eB : eF;
-                const uint4 T = dir ? TB : TF;
-                const uint32_t lay = dir ? layB : layF;
-                const uint32_t idx = dir ? bi : fi;
-                const uint64_t ts = dir ? tB : tF;
-                const uint64_t st = ts > tlast ? ts : tlast;
-                const uint64_t end = st + (uint64_t)lay * (dir ? T.y : T.x);
-                busy += end - st;
-                tlast = end;
-                const uint32_t act = lay * T.z;
-                cur = dir ? cur - act : cur + act;
-                peak = cur > peak ? cur : peak;
-                const bool wrapP = dir ? isFirst : isLast;
-                // one lane places, so the publication can branch freely: a plain channel write for
-                // interior ranks, the wrap-slot read-modify-write only at rank 0 / P-1
-                if (!wrapP) {
-                    uint64_t *pa = &ringAll[(idx & (D - 1)) * P + (dir ? colOut1 : colOut0)];
-                    const uint64_t pold = *pa;
-                    *pa = end;
-                    const uint32_t ccnt = dir ? bu : fd;                     // consumer neighbour's count
-                    if (idx >= ccnt + D) spill_keep(spill, dir, r, P, n_max, idx, pold);
-                } else {
-                    uint64_t *pa = &depAll[min(e.y >> 16, SINK)];
-                    const uint64_t pold = *pa;
-                    const int32_t sgn = (int32_t)(e.x << 6) >> 30;
-                    const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
-                    const uint64_t cand2 = (pold & HIGH_MASK) | pv;
-                    *pa = (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT);
-                    if (e.x & E_MULTI) {
-                        const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
-                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
-                        const uint32_t msk = dir ? mi[i].prod_mask : mi[i].cons_mask;
-                        for (uint32_t c = 0; c < nmod; c++) {
-                            if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
-                            uint64_t *sl = &depAll[dir ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
-                            const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
-                            *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                // the placement, specialised per direction at compile time (one lane runs it, so the
+                // branch on dir costs nothing and the F / B selects disappear)
+                auto place = [&](auto dirc) {
+                    constexpr uint32_t DIR = decltype(dirc)::value;
+                    const uint2 e = DIR ? eB : eF;
+                    const uint4 T = DIR ? TB : TF;
+                    const uint32_t lay = DIR ? layB : layF;
+                    const uint32_t idx = DIR ? bi : fi;
+                    const uint64_t ts = DIR ? tB : tF;
+                    const uint64_t st = ts > tlast ? ts : tlast;
+                    const uint64_t end = st + (uint64_t)lay * (DIR ? T.y : T.x);
+                    busy += end - st;
+                    tlast = end;
+                    const uint32_t act = lay * T.z;
+                    cur = DIR ? cur - act : cur + act;
+                    peak = cur > peak ? cur : peak;
+                    const bool wrapP = DIR ? isFirst : isLast;
+                    // a plain channel write for interior ranks, the wrap-slot read-modify-write only
+                    // at rank 0 / P-1
+                    if (!wrapP) {
+                        uint64_t *pa = &ringAll[(idx & (D - 1)) * P + (DIR ? colOut1 : colOut0)];
+                        const uint64_t pold = *pa;
+                        *pa = end;
+                        const uint32_t ccnt = DIR ? bu : fd;                 // consumer neighbour's count
+                        if (idx >= ccnt + D) spill_keep(spill, DIR, r, P, n_max, idx, pold);
+                    } else {
+                        uint64_t *pa = &depAll[min(e.y >> 16, SINK)];
+                        const uint64_t pold = *pa;
+                        const int32_t sgn = (int32_t)(e.x << 6) >> 30;
+                        const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
+                        const uint64_t cand2 = (pold & HIGH_MASK) | pv;
+                        *pa = (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT);
+                        if (e.x & E_MULTI) {
+                            const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
+                            const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
+                            const uint32_t msk = DIR ? mi[i].prod_mask : mi[i].cons_mask;
+                            for (uint32_t c = 0; c < nmod; c++) {
+                                if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                                uint64_t *sl = &depAll[DIR ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
+                                const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
+                                *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                            }
                         }
                     }
-                }
+                };
+                if (dir) place(std::integral_constant<uint32_t, 1>());
+                else place(std::integral_constant<uint32_t, 0>());
                 const uint32_t t = fi + bi;
                 if (dir) wbuf |= 1u << (t & 31);
                 if ((t & 31) == 31 || t + 1 == S2) { fbOut[(t >> 5) * P] = wbuf; wbuf = 0; }
