@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         uint32_t layF = 0, layB = 0;
         uint64_t tF = 0, tB = 0;
         bool rdyF = false, rdyB = false, needF = true, needB = true;
+        uint32_t fstep = 0;
         for (;;) {
             const uint32_t fu = __shfl_up_sync(FULL, fi, 1, G), bu = __shfl_up_sync(FULL, bi, 1, G);
             const uint32_t fd = __shfl_down_sync(FULL, fi, 1, G), bd = __shfl_down_sync(FULL, bi, 1, G);
@@ -528,16 +529,21 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             uint64_t key = tmin == INF ? INF : (tmin << 5) | (uint64_t)r;
             uint64_t gk = group_min<G>(key);
             bool relax = false;
-            if (__any_sync(FULL, gk == INF)) {             // stuck only because of gates? lift them (R-31)
+            // (a whole-warp group's gk is warp-uniform: no vote needed)
+            if (G == 32 ? gk == INF : __any_sync(FULL, gk == INF)) {   // stuck only because of gates? (R-31)
                 const uint64_t k2 = rdyF ? ((tF << 5) | (uint64_t)r) : INF;
                 const uint64_t g2 = group_min<G>(k2);      // every lane shuffles; stuck groups use it
                 if (gk == INF) { gk = g2; relax = true; }
             }
-            const uint32_t alive = __ballot_sync(FULL, !done);
-            if (alive == 0) break;
-            if (gk == INF && (alive & gmask)) {            // no rank of this group can place a stage: a cycle
-                dl = true;
-                done = true;
+            // exit / cycle checks (every 8th step for a whole-warp group: a step without a placement
+            // repeats forever, so the verdict is exact; a finished group idles at most 7 steps)
+            if (G < 32 || (++fstep & 7) == 0) {
+                const uint32_t alive = __ballot_sync(FULL, !done);
+                if (alive == 0) break;
+                if (gk == INF && (alive & gmask)) {        // no rank of this group can place a stage: a cycle
+                    dl = true;
+                    done = true;
+                }
             }
             __syncwarp();
             uint32_t pdir = 0;
