@@ -49,8 +49,11 @@ class _OCands(ctypes.Structure):
 def _load():
     global _lib
     if _lib is None:
-        build()
-        lib = ctypes.CDLL(_SO)
+        path = os.environ.get("ORACLE_LIB")        # e.g. a sanitizer build (tests/test_sanitizers.py)
+        if not path:
+            build()
+            path = _SO
+        lib = ctypes.CDLL(path)
         lib.oracle_chunk_layers.restype = ctypes.c_int
         lib.oracle_chunk_layers.argtypes = [ctypes.c_uint32] * 3 + [ctypes.c_void_p]
         lib.oracle_split.restype = ctypes.c_int
