@@ -88,7 +88,7 @@ def test_h2_two_module_join_timeline():
 @pytest.mark.parametrize("tf,tb", [(1, 1), (1, 2), (2, 3)])
 def test_1f1b_and_gpipe_closed_forms(tf, tb):
     # 1F1B / GPipe with uniform stages: makespan (m+P-1)(t_f+t_b), bubble (P-1)/(m+P-1)
-    # (P=4, m=64 -> 4.4776%), 1F1B peaks min(P-r, m)*a, GPipe peaks m*a.
+    # (P=4, m=64 -> "≈ 4.48%" = 3/67), 1F1B peaks min(P-r, m)*a, GPipe peaks m*a.
     a = 3
     for P in range(1, 7):
         for m in range(1, 9):
@@ -105,11 +105,11 @@ def test_1f1b_and_gpipe_closed_forms(tf, tb):
 
 
 def test_spec_1f1b_bubble_example():
-    # P=4, n=64, uniform -> bubble (P-1)/(n+P-1) = 3/67 = 4.4776%
+    # P=4, n=64, uniform -> bubble (P-1)/(n+P-1) "≈ 4.48%" (exactly 3/67 = 4.4776...%)
     pb = H.uniform_problem(4, 64, 1, 2)
     cs = H.candidates_from_orders(pb, [[1] * 64], [H.one_f_one_b(4, 64)])
     r = ev(pb, cs)
-    assert round(r.bubble[0] * 100, 4) == 4.4776 and r.bubble[0] == 3 / 67
+    assert round(r.bubble[0] * 100, 2) == 4.48 and r.bubble[0] == 3 / 67
 
 
 # ---------------------------------------------------------------- A.4 ---------
