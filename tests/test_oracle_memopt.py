@@ -1,11 +1,11 @@
 """Pins of the oracle's per-layer memory optimisation (M1-M4, §5.3).
 
-* M2 candidates: the worked examples of SPEC.md:411-416 ("2 layers x {none: (10 ms, 8 GB),
+* M2 candidates: the worked examples of SPEC.md:416-417 ("2 layers x {none: (10 ms, 8 GB),
   checkpoint: (13 ms, 2 GB)}, S=3 -> {(20 ms, 16 GB), (23 ms, 10 GB), (26 ms, 4 GB)}"; "1 layer,
   2 strategies, S=10 -> exactly 2 candidates"), and properties against brute force over every
   per-layer assignment: extremes present, Pareto order, size <= S, and the bucket guarantee
   (every combination is matched by a candidate no slower and at most one bucket width larger);
-* M3 selection: SPEC.md:419-424's one-pair examples (M = 10 GB -> the 8 GB candidate, M = 12 GB ->
+* M3 selection: SPEC.md:425-426's one-pair examples (M = 10 GB -> the 8 GB candidate, M = 12 GB ->
   the 6 ms one); unbounded memory -> every pair at its fastest candidate, whose re-timed makespan
   equals the fixed-order oracle run on the fastest strategy's tables; on generated schedules an
   independent re-check of feasibility at every forward slot and of the greedy's termination

@@ -1,7 +1,7 @@
 """Pins of the oracle's MCTS segment reordering (S1-S6, §5.1).
 
 * exhaustive budget on a tiny instance -> the brute-force optimum over every class order
-  (S:397 "exhaustive budget -> ... equal to brute force"), the brute force built here with an
+  (S:399 "exhaustive budget -> ... equal to brute force"), the brute force built here with an
   independent priority -> queue-order builder and the (pinned) oracle interleaving;
 * the best-so-far trace never decreases;
 * the reported best schedule re-scores to the reported makespan with the fixed-order oracle;
