@@ -167,8 +167,7 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                                                                             //   slot of the q-th backward
     int32_t *cb = reinterpret_cast<int32_t *>(dms + n_max);                 // [n_max] ctab row of pair p
     uint16_t *eP = reinterpret_cast<uint16_t *>(cb + n_max);                // end of pair p's point range
-    uint16_t *qp = eP + n_max;                                              // backward position of pair p
-    uint8_t *cur = reinterpret_cast<uint8_t *>(qp + n_max);                 // selected candidate
+    uint8_t *cur = reinterpret_cast<uint8_t *>(eP + n_max);                 // selected candidate
     uint8_t *ncand = cur + n_max;
     uint8_t *Mb = ncand + n_max;                                            // [nq]
 
@@ -255,7 +254,6 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 if (q == 0xFFFFu) { bad = true; continue; }
                 const uint32_t e = (uint32_t)bsl[q] - q;
                 eP[p] = (uint16_t)e;
-                qp[p] = (uint16_t)q;
                 const uint32_t dc = __ldg(&segdec[s]);
                 const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
                 const uint32_t qq = b * nmod + i, M = Mb[qq];
@@ -348,10 +346,15 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 __syncwarp();
             }
         }
+        // the backward row needs each pair's backward position again: rebuild the segment -> position
+        // map from the record into the (now dead) step arrays
+        for (uint32_t q = lane; q < n; q += 32)
+            invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_bwd) + q)] = (uint16_t)q;
+        __syncwarp();
         for (uint32_t p = lane; p < n_max; p += 32) {
             const uint8_t c = p < n ? cur[p] : 0;
             selF[p] = c;
-            if (p < n) selB[qp[p]] = c;
+            if (p < n) selB[invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_fwd) + p)]] = c;
         }
         if (n < n_max)
             for (uint32_t q = n + lane; q < n_max; q += 32) selB[q] = 0;
