@@ -180,7 +180,8 @@ dip_status dip_interleave(const dip_model *m, dip_workspace *w, void *d_records,
  * smallest, fastest of each of S-2 memory buckets; Pareto, memory ascending). 1 <= n_strat <= 8,
  * 2 <= S <= 16. DIP_ERANGE if a pair total exceeds u32, the enumeration exceeds 2^20 count
  * vectors per pair, the menu yields two candidates of equal memory or latency, or a rank's budget
- * plus n_max x the largest candidate memory reaches 2^31 KiB (the selection works in int32). Replaces a
+ * plus n_max x the largest candidate memory reaches 2^31 KiB (the selection works in int32), or the
+ * candidate table exceeds 65535 rows of S entries. Replaces a
  * previous menu. Synchronous. Device model only. */
 dip_status dip_set_strategies(dip_model *m, uint32_t n_strat, const uint32_t *f_ns, const uint32_t *b_ns,
                               const uint32_t *act_kib, uint32_t S);

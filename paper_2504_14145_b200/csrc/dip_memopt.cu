@@ -165,11 +165,10 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
     uint16_t *invB = fw + n_max;                                            //   written: forward sequence,
     uint16_t *bsl = invB + n_max;                                           //   segment -> backward position,
                                                                             //   slot of the q-th backward
-    int32_t *cb = reinterpret_cast<int32_t *>(dms + n_max);                 // [n_max] ctab row of pair p
-    uint16_t *eP = reinterpret_cast<uint16_t *>(cb + n_max);                // end of pair p's point range
-    uint8_t *cur = reinterpret_cast<uint8_t *>(eP + n_max);                 // selected candidate
-    uint8_t *ncand = cur + n_max;
-    uint8_t *Mb = ncand + n_max;                                            // [nq]
+    uint16_t *cbr = reinterpret_cast<uint16_t *>(dms + n_max);              // [n_max] ctab row / S of pair p
+    uint16_t *eP = cbr + n_max;                                             // end of pair p's point range
+    uint8_t *cn = reinterpret_cast<uint8_t *>(eP + n_max);                  // selected candidate | (count-1) << 4
+    uint8_t *Mb = cn + n_max;                                               // [nq]
 
     const int32_t INF = 0x7FFFFFFF;
     for (;;) {
@@ -259,10 +258,9 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 const uint32_t qq = b * nmod + i, M = Mb[qq];
                 const uint32_t W = __ldg(&wtab[__ldg(&woff[qq]) + M * (M - 1) / 2 + j]);
                 const int32_t row = __ldg(&kp.crow[__ldg(&mi[i].lay_off) + k * P + r]) + (int32_t)((__ldg(&mi[i].tab_off) + W) * S);
-                cb[p] = row;
+                cbr[p] = (uint16_t)((uint32_t)row / S);   // rows are S-aligned; < 65536 rows (host guard)
                 const uint4 E = __ldg(&kp.ctab[row]);
-                ncand[p] = (uint8_t)E.w;
-                cur[p] = 0;
+                cn[p] = (uint8_t)((E.w - 1u) << 4);      // candidate 0, E.w candidates (1..16)
                 if (e > p) {
                     atomicAdd(&slack[p], (int32_t)E.z);
                     if (e < n) atomicSub(&slack[e], (int32_t)E.z);
@@ -304,9 +302,10 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             // shuffle tournament
             for (uint32_t p = lane; p < n; p += 32) {
                 uint32_t k = 0, dm = 0;
-                if (ncand[p] > 1) {
-                    k = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[p]])) << 16) | (0xFFFFu - p);
-                    dm = __ldg(&kp.ctab[cb[p] + 1]).z - __ldg(&kp.ctab[cb[p]]).z;
+                if ((cn[p] >> 4) > 0) {
+                    const uint32_t cb = (uint32_t)cbr[p] * S;
+                    k = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb])) << 16) | (0xFFFFu - p);
+                    dm = __ldg(&kp.ctab[cb + 1]).z - __ldg(&kp.ctab[cb]).z;
                 }
                 key[p] = k;
                 dms[p] = dm;
@@ -333,12 +332,12 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 }
                 for (uint32_t k = a0 + lane; k < a1; k += 32) slack[k] -= (int32_t)bdm;
                 if (lane == 0) {
-                    const uint32_t c = cur[a0] + 1u;
-                    cur[a0] = (uint8_t)c;
+                    const uint32_t v = cn[a0], c = (v & 15u) + 1u, cb = (uint32_t)cbr[a0] * S;
+                    cn[a0] = (uint8_t)((v & 0xF0u) | c);
                     uint32_t k = 0, dm = 0;
-                    if (c + 1u < ncand[a0]) {
-                        k = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb[a0] + c])) << 16) | (0xFFFFu - a0);
-                        dm = __ldg(&kp.ctab[cb[a0] + c + 1]).z - __ldg(&kp.ctab[cb[a0] + c]).z;
+                    if (c < (v >> 4)) {                      // c + 1 < count
+                        k = ((0xFFFFu - (uint32_t)__ldg(&kp.srank[cb + c])) << 16) | (0xFFFFu - a0);
+                        dm = __ldg(&kp.ctab[cb + c + 1]).z - __ldg(&kp.ctab[cb + c]).z;
                     }
                     key[a0] = k;
                     dms[a0] = dm;
@@ -352,7 +351,7 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_bwd) + q)] = (uint16_t)q;
         __syncwarp();
         for (uint32_t p = lane; p < n_max; p += 32) {
-            const uint8_t c = p < n ? cur[p] : 0;
+            const uint8_t c = p < n ? (cn[p] & 15u) : 0;
             selF[p] = c;
             if (p < n) selB[invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_fwd) + p)]] = c;
         }

@@ -57,7 +57,8 @@ extern "C" dip_status dip_set_strategies(dip_model *M, uint32_t n_strat, const u
             crow[row] = (int32_t)t_base[t] - (int32_t)(M->tab_off[i] * S);
         }
     }
-    if ((uint64_t)base >= (1ull << 31)) return fail(DIP_ERANGE, "candidate table too large");
+    if ((uint64_t)base >= (1ull << 31) || base / S >= 65536u)   // the selection keeps u16 row indices
+        return fail(DIP_ERANGE, "candidate table too large");
     // device buffers
     std::vector<void *> tmp;
     auto cleanup = [&]() { for (void *p : tmp) cudaFree(p); };
@@ -166,7 +167,7 @@ extern "C" dip_status dip_set_strategies(dip_model *M, uint32_t n_strat, const u
     M->kp.S = S;
     // selection kernel shape: 4 warps per block, per-warp working set in shared memory
     const uint32_t nmx = M->n_max, nq = M->m * nm;
-    M->mo_warp_bytes = up16(4 * ((nmx + 1) & ~1u) + nmx * (8 + 4 + 2 + 1 + 1) + nq);
+    M->mo_warp_bytes = up16(4 * ((nmx + 1) & ~1u) + nmx * (8 + 2 + 2 + 1) + nq);
     const size_t smem = 4 * (size_t)M->mo_warp_bytes;
     cudaDeviceProp prop;
     CUDA_TRY(cudaGetDeviceProperties(&prop, M->device));
