@@ -296,6 +296,8 @@ class Comm:
 
 
 def eval_schedules(model: Model, ws: Workspace, d_records, count: int, d_results, d_peaks=None, stream=None):
+    """§8(a2)-(a6): score `count` device records (d_results: count x 24 B; d_peaks: [count, P] u32 or
+    None) on `stream`, asynchronously; the fused argmin key is left in the workspace for argmin()."""
     _check(lib().dip_eval_schedules(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results),
                                     _ptr(d_peaks), _stream(stream)), "dip_eval_schedules")
 
@@ -369,6 +371,8 @@ def validate_plan(model: Model, record, acts, off):
 
 def argmin(model: Model, ws: Workspace, count: int, shard_stride: Optional[int] = None, rank: int = 0,
            world: int = 1, comm: Optional[Comm] = None, stream=None) -> Winner:
+    """§8(a7): the winner of the last scoring call -- lowest (makespan, global index) among status-OK
+    candidates, across ranks through one NCCL allreduce when `comm` is given. Synchronous."""
     w = _Winner()
     _check(lib().dip_argmin(model.handle, ws.handle, count, shard_stride if shard_stride is not None else count,
                             rank, world, comm.handle if comm else None, ctypes.byref(w), _stream(stream)),
@@ -378,6 +382,8 @@ def argmin(model: Model, ws: Workspace, count: int, shard_stride: Optional[int] 
 
 def eval_host(model: Model, ws: Workspace, h_records, count: int, h_results=None, shard_stride: Optional[int] = None,
               rank: int = 0, world: int = 1, comm: Optional[Comm] = None, stream=None) -> Winner:
+    """End to end from host records (pinned for overlap): chunked H2D overlapped with scoring on two
+    streams, then argmin(). h_results (host, count x 24 B) may be None. Synchronous."""
     w = _Winner()
     _check(lib().dip_eval_host(model.handle, ws.handle, _ptr(h_records), count, _ptr(h_results),
                                shard_stride if shard_stride is not None else count, rank, world,
@@ -393,6 +399,7 @@ def pack_key(makespan_ns: int, rank: int, local: int, shard_stride: int, world: 
 
 
 def unpack_key(key: int, shard_stride: int, world: int) -> Winner:
+    """Inverse of pack_key (UINT64_MAX -> not found)."""
     w = _Winner()
     _check(lib().dip_unpack_key(key, shard_stride, world, ctypes.byref(w)), "dip_unpack_key")
     return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
