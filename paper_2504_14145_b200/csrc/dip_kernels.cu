@@ -116,6 +116,7 @@ constexpr uint64_t HIGH_MASK = ~VAL_MASK;
 
 
 
+
 // rare paths kept out of line (a call is never if-converted into the round's common path)
 __device__ __noinline__ uint64_t spill_load(const unsigned long long *spill, uint32_t d, uint32_t r, uint32_t P,
                                             uint32_t n_max, uint32_t idx) {
@@ -421,24 +422,26 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 busy += lat;
                 cur = d ? cur - act : cur + act;
                 peak = cur > peak ? cur : peak;
-                const int32_t sgn = (int32_t)(e.x << 6) >> 30;                 // publish factor -1 / 0 / +1
-                const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
-                const uint64_t cand = (pold & HIGH_MASK) | pv;
-                const uint64_t rmw = (cand > pold ? cand : pold) + (1ull << PEND_SHIFT);
-                *pa = wrapP ? rmw : end;
                 if (!wrapP) {
+                    *pa = end;
                     const uint32_t cc = d ? bu : fd;                       // consumer neighbour's count
                     if (idx >= cc + D)                    // consumer is >= D behind: keep the old entry
                         spill_keep(spill, d, r, P, n_max, idx, pold);
-                } else if (e.x & E_MULTI) {               // several join targets (rare); the plain store hit SINK
-                    const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
-                    const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
-                    const uint32_t msk = d ? mi[i].prod_mask : mi[i].cons_mask;
-                    for (uint32_t c = 0; c < nmod; c++) {
-                        if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
-                        uint64_t *sl = &depAll[d ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
-                        const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
-                        *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                } else {                                  // rank 0 / P-1: the wrap slot's read-modify-write
+                    const int32_t sgn = (int32_t)(e.x << 6) >> 30;             // publish factor -1 / 0 / +1
+                    const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
+                    const uint64_t cand = (pold & HIGH_MASK) | pv;
+                    *pa = (cand > pold ? cand : pold) + (1ull << PEND_SHIFT);
+                    if (e.x & E_MULTI) {           // several join targets (rare); the plain store hit SINK
+                        const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
+                        const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
+                        const uint32_t msk = d ? mi[i].prod_mask : mi[i].cons_mask;
+                        for (uint32_t c = 0; c < nmod; c++) {
+                            if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
+                            uint64_t *sl = &depAll[d ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
+                            const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
+                            *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
+                        }
                     }
                 }
                 if (d) cB++; else cF++;
