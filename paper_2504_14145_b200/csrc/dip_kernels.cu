@@ -114,9 +114,6 @@ constexpr uint32_t E_MULTI = 4u << 24;    // several join targets: slower loop (
 //   slot = max(slot, (slot & HIGH) | value) + (1 << 56)
 constexpr uint64_t HIGH_MASK = ~VAL_MASK;
 
-#ifndef DIP_KX
-#define DIP_KX 0   // A/B: the scorer reads a publication's old slot value only where it is needed
-#endif
 
 
 
@@ -382,15 +379,11 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];       // done lanes: a safe row
             const uint32_t ring = (idx & (D - 1)) * P;
             const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (d ? colIn1 : colIn0)];
-#if !DIP_KX
             uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)] : &ringAll[ring + (d ? colOut1 : colOut0)];
-#endif
             const uint4 T = tab[e.x & 0xFFFu];
             const uint32_t lay = layers[((e.x >> 12) & 0xFFFu) + r];
             const uint64_t v = *ca;
-#if !DIP_KX
             const uint64_t pold = *pa;
-#endif
             // a ready value has a zero pending byte, so it needs no mask (v < 2^56 <=> high word < 2^24)
             const bool ready = !done && nb > idx && (uint32_t)(v >> 32) < (1u << 24);
             const uint32_t w = (wrapC && !d) ? 0u : T.w;   // rank 0's F wrap slot already holds + p2p
@@ -430,24 +423,12 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
                 busy += lat;
                 cur = d ? cur - act : cur + act;
                 peak = cur > peak ? cur : peak;
-#if DIP_KX
-                if (!wrapP) {                             // own channel column: read the old entry only to spill it
-                    uint64_t *pa = &ringAll[ring + (d ? colOut1 : colOut0)];
-                    const uint32_t cc = d ? bu : fd;                       // consumer neighbour's count
-                    if (idx >= cc + D)                    // consumer is >= D behind: keep the old entry
-                        spill_keep(spill, d, r, P, n_max, idx, *pa);
-                    *pa = end;
-                } else {                                  // rank 0 / P-1: the wrap slot's read-modify-write
-                    uint64_t *pa = &depAll[min(e.y >> 16, SINK)];
-                    const uint64_t pold = *pa;
-#else
                 if (!wrapP) {
                     *pa = end;
                     const uint32_t cc = d ? bu : fd;                       // consumer neighbour's count
                     if (idx >= cc + D)                    // consumer is >= D behind: keep the old entry
                         spill_keep(spill, d, r, P, n_max, idx, pold);
                 } else {                                  // rank 0 / P-1: the wrap slot's read-modify-write
-#endif
                     const int32_t sgn = (int32_t)(e.x << 6) >> 30;             // publish factor -1 / 0 / +1
                     const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
                     const uint64_t cand = (pold & HIGH_MASK) | pv;
