@@ -14,6 +14,11 @@
  * + a shared forward and a shared backward segment sequence + a
  * per-rank forward/backward interleaving (reading R-1 of DESIGN.md).
  *
+ * Beyond the scorer, the planner's other steps: dip_interleave (§5.2 dual-queue
+ * interleaving), dip_search (§5.1 MCTS with batched GPU rollouts), dip_set_strategies /
+ * dip_strategy_candidates / dip_memopt (§5.3 per-layer memory optimisation), dip_timeline /
+ * dip_compile_plan / dip_validate_plan (§6.3 execution plans).
+ *
  * Units: time in integer nanoseconds (u64 accumulators), memory in KiB (u32).
  * All calls return dip_status (0 = DIP_OK); no C++ exception crosses the ABI.
  * Per-candidate problems are DATA (dip_result.status), never call errors.
