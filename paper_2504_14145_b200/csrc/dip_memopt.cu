@@ -13,10 +13,10 @@
 //    difference array + warp scan, then runs the greedy: every lane proposes its best pair
 //    (largest latency saving per KiB, ties to the lower p, as a 32-bit key built from the host's
 //    exact ranking of all steps of the candidate table), one REDUX picks the winner, and only
-//    then is the winner's step checked
-//    against the range minimum of the slack (lanes over its points): if it fits the lanes subtract
-//    it, else the pair is blocked for good (the slack never grows), which makes this lazy order
-//    pick exactly the oracle's "best feasible pair". Output: sel[x][r][0][p] / [1][q].
+//    then is the winner's step checked against the range minimum of the slack (lanes over its
+//    points): if it fits the lanes subtract it, else the pair is blocked for good (the slack never
+//    grows), which makes this lazy order pick exactly the oracle's "best feasible pair".
+//    17 B of shared memory per segment (32 warps/SM for 94B). Output: sel[x][r][0][p] / [1][q].
 //  The re-timing with the selected candidates (M4) is the scorer's MODE 3 (dip_kernels.cu).
 #include <cstdint>
 
