@@ -107,3 +107,13 @@ def test_interleave_bench_size_sampled():
     assert np.array_equal(res["makespan_ns"][idx], ref.makespan)
     assert np.array_equal(res["bubble"][idx].view(np.uint64), ref.bubble.view(np.uint64))
     assert np.array_equal(pk[idx].astype(np.uint64), ref.peaks)
+
+
+def test_interleave_gating_and_gate_lifting_on_gpu():
+    # the hand-worked one-rank cases of tests/test_oracle_interleave.py (ungated, gated, gate lifted)
+    for budget, order in [(10, "FFBB"), (5, "FBFB"), (4, "FBFB")]:
+        pb = H.uniform_problem(1, 2, 1, 2, act=5, budget=[budget])
+        cs = H.candidates_from_orders(pb, [[1, 1]], [[[("F", 0), ("F", 1), ("B", 0), ("B", 1)]]])
+        res, pk, bits, win, _, _ = run_interleave(pb, cs)
+        assert "".join("B" if (int(bits[0, 0, 0]) >> t) & 1 else "F" for t in range(4)) == order
+        check(pb, cs)

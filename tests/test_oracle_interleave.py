@@ -96,3 +96,19 @@ def test_bad_and_deadlocked_priority_orders():
     c2.fwd[0, :2] = [1, 0]
     bits, r = oracle.interleave(pb2, c2)
     assert r.status[0] == DL
+
+
+@pytest.mark.parametrize("budget,order,status,peak", [
+    (10, "FFBB", OK, 10),      # ungated: F1 (t_start 0) precedes B0 (t_start t_f): step 4, smallest t_start
+    (5, "FBFB", OK, 5),        # gated (R-30): the second forward would exceed the budget
+    (4, "FBFB", OOM, 5)])      # every rank blocked by its gate only -> the gate is lifted (R-31)
+def test_gating_and_gate_lifting_by_hand(budget, order, status, peak):
+    # one rank, two microbatches, t_f = 1, t_b = 2, 5 KiB of activation per forward; worked by hand
+    # from P:532-548: step 1 places F0; step 2 compares F1 (t_start 0) and B0 (t_start 1 = end of F0)
+    pb = H.uniform_problem(1, 2, 1, 2, act=5, budget=[budget])
+    cs = H.candidates_from_orders(pb, [[1, 1]], [[[("F", 0), ("F", 1), ("B", 0), ("B", 1)]]])
+    bits, r = oracle.interleave(pb, cs)
+    got = "".join("B" if (int(bits[0, 0, 0]) >> t) & 1 else "F" for t in range(4))
+    assert got == order
+    assert r.status[0] == status and int(r.peaks[0, 0]) == peak
+    assert int(r.makespan[0]) == 2 * (1 + 2)
