@@ -78,7 +78,10 @@ def _load():
         lib.oracle_memopt.restype = ctypes.c_int
         lib.oracle_memopt.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32] + [ctypes.c_void_p] * 3 + \
             [ctypes.c_uint32, ctypes.POINTER(_OCands), ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 7 + \
-            [ctypes.c_int]
+            [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
+        lib.oracle_select_rank.restype = ctypes.c_int
+        lib.oracle_select_rank.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 4 + \
+            [ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_argmin.restype = ctypes.c_int64
         lib.oracle_argmin.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64]
         _lib = lib
@@ -223,11 +226,38 @@ def mem_candidates(f, b, act, layers: int, S: int):
     return [tuple(int(v) for v in out[x]) for x in range(k)]
 
 
-def memopt(pb, cands, menu, S: int = 10, first: int = 0, count: Optional[int] = None, threads: int = 1):
+def select_rank(sF, sB, cands, budget: int, gap_pm: int = 50, node_cap: int = 4096):
+    """M3 on one rank: pairs in forward order with slots sF[p] < ... and backward slots
+    sB[p]; cands[p] = [(F, B, mem), ...] sorted by memory ascending. Returns (selection, stats)
+    with stats = dict(warm, bound, final, nodes, infeasible, certified, capped)."""
+    n = len(sF)
+    Sst = max([len(c) for c in cands] + [1])
+    arr = np.zeros((max(n, 1), Sst, 3), np.uint64)
+    nc = np.zeros(max(n, 1), np.uint32)
+    for p, cl in enumerate(cands):
+        nc[p] = len(cl)
+        for c, v in enumerate(cl):
+            arr[p, c] = v
+    f = np.ascontiguousarray(sF, np.uint32)
+    b = np.ascontiguousarray(sB, np.uint32)
+    cur = np.zeros(max(n, 1), np.uint32)
+    st = np.zeros(5, np.uint64)
+    _load().oracle_select_rank(n, f.ctypes.data, b.ctypes.data, nc.ctypes.data, arr.ctypes.data, Sst, int(budget),
+                               gap_pm, node_cap, cur.ctypes.data, st.ctypes.data)
+    fl = int(st[4])
+    return [int(v) for v in cur[:n]], {"warm": int(st[0]), "bound": int(st[1]), "final": int(st[2]),
+                                       "nodes": int(st[3]), "infeasible": bool(fl & 1),
+                                       "certified": bool(fl & 2), "capped": bool(fl & 4)}
+
+
+def memopt(pb, cands, menu, S: int = 10, first: int = 0, count: Optional[int] = None, threads: int = 1,
+           gap_pm: int = 50, node_cap: int = 4096, stats: bool = False):
     """M1-M4: per-layer memory optimisation of each candidate schedule. `menu` =
     (f, b, act) arrays [n_strat, T] aligned with the model's tables. Returns (sel, Results) with
     sel [count, P, 2, n_max] the selected candidate index of each pair at forward position p
-    (sel[..., 0, p]) and backward position q (sel[..., 1, q]) and the re-timed results."""
+    (sel[..., 0, p]) and backward position q (sel[..., 1, q]) and the re-timed results. M3 solves
+    each rank's ILP to a relative gap <= gap_pm per mille, at most node_cap B&B children.
+    With stats=True also returns [count, P, 5] per-rank (warm, bound, final, nodes, flags)."""
     if count is None:
         count = cands.count - first
     f, b, a = (np.ascontiguousarray(v, np.uint32) for v in menu)
@@ -235,12 +265,14 @@ def memopt(pb, cands, menu, S: int = 10, first: int = 0, count: Optional[int] = 
     bd = _Bound(pb, cands)
     res = Results(count, pb.P)
     sel = np.zeros((count, pb.P, 2, pb.n_max), np.uint8)
+    rst = np.zeros((count, pb.P, 5), np.uint64) if stats else None
     rc = lib.oracle_memopt(ctypes.byref(bd.pb), f.shape[0], f.ctypes.data, b.ctypes.data, a.ctypes.data, S,
                            ctypes.byref(bd.cs), first, count, sel.ctypes.data, res.makespan.ctypes.data,
                            res.status.ctypes.data, res.oom_mask.ctypes.data, res.bubble.ctypes.data,
-                           res.peaks.ctypes.data, res.busy.ctypes.data, threads)
+                           res.peaks.ctypes.data, res.busy.ctypes.data, threads, gap_pm, node_cap,
+                           None if rst is None else rst.ctypes.data)
     assert rc == 0
-    return sel, res
+    return (sel, res, rst) if stats else (sel, res)
 
 
 def argmin(makespan: np.ndarray, status: np.ndarray) -> int:

@@ -663,9 +663,10 @@ typedef struct { int parent, cls, depth, nch, cap; int *ch; double s; uint32_t N
 typedef struct {
     uint32_t n_strat, S;
     const uint32_t *f, *b, *act;    /* [n_strat][tab_off[nmod]] per-layer menu (M1) */
+    uint32_t gap_pm, node_cap;      /* M3: optimality gap in per mille, B&B child budget */
 } omenu;
 static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, uint64_t x, uint8_t *sel,
-                       ores *res, uint64_t *peaks);
+                       ores *res, uint64_t *peaks, uint64_t *rstats);
 
 /* S2: queue order of one direction from class priorities (plain selection, O(n^2)) */
 static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *base, const int *clsof, uint32_t C,
@@ -735,7 +736,7 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
                   double *trace, double *best_score, uint64_t *best_makespan, uint16_t *best_fwd,
                   uint16_t *best_bwd, uint32_t *best_bits, uint64_t *scored_out,
                   uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma, uint32_t S) {
-    omenu mn = {n_strat, S, mf, mb, ma};   /* n_strat = 0: rollouts are interleaved only */
+    omenu mn = {n_strat, S, mf, mb, ma, 50, 4096};   /* n_strat = 0: rollouts are interleaved only */
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
     uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
     int *clsof = malloc(sizeof(int) * m * nm);
@@ -853,7 +854,7 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
                 ocands c1 = {n_max, fbw, spl + (size_t)x * m * nm, nn_ + x, fw + (size_t)x * n_max,
                              bw + (size_t)x * n_max, bits + (size_t)x * P * fbw};
                 uint8_t *sel = malloc((size_t)P * 2 * n_max);
-                memopt_one(pb, &mn, &c1, 0, sel, &r, NULL);
+                memopt_one(pb, &mn, &c1, 0, sel, &r, NULL, NULL);
                 free(sel);
             }
             double sc = r.status == ST_OK ? LB / (double)r.makespan : 0.0;
@@ -908,14 +909,25 @@ int64_t oracle_argmin(const uint64_t *makespan, const uint32_t *status, uint64_t
  *      identical, so a combination is fixed by how many layers take each strategy). Ties: less
  *      memory, then the smaller forward latency. Duplicates and dominated entries dropped;
  *      sorted by memory ascending (so latency strictly decreases).
- *   M3 selection on each rank: pairs i with interval [slot of F, slot of B) in
- *      the rank's order; at every forward slot s_k the selected memory of the pairs live there
- *      must stay <= the rank's budget M. The warm start ("greedy initial solution"):
- *      start from candidate 0 everywhere (the min-memory one, feasible iff the schedule is not
- *      OOM; if it is, nothing changes), then repeatedly move the pair with the largest
- *      latency saving per KiB of extra memory (next candidate; ties: earliest forward slot) to
- *      its next candidate as long as every point it covers keeps slack; the ILP refinement
- *      with a <= 5 % gap is out of scope.
+ *   M3 selection on each rank, the ILP of P:572-582: pairs i with interval
+ *      [slot of F, slot of B) in the rank's order; minimise sum_i lat_i (lat = F + B of the
+ *      selected candidate) subject to: at every forward slot s_k the selected memory of the pairs
+ *      live there stays <= the rank's budget M. Solved as P:584-590 describes, to a relative
+ *      optimality gap <= gap (default 5 %), warm-started by a greedy:
+ *      M3a warm start: candidate 0 everywhere (the min-memory one, feasible iff the schedule is
+ *          not OOM; if it is, nothing changes and M3b/M3c are skipped), then repeatedly move the
+ *          pair with the largest latency saving per KiB of extra memory (next candidate; ties:
+ *          earliest forward slot) to its next candidate as long as every point it covers keeps
+ *          slack.
+ *      M3b lower bound (the solver's relaxation bound, reading R-39): a Lagrangian relaxation of
+ *          the memory constraints at the points K* where the warm start blocks a pair, with one
+ *          multiplier mu found by bisection (fixed point 2^-16); every pair then picks its
+ *          candidate independently and the bound is ceil(L(mu)), valid for any mu >= 0.
+ *      M3c branch and bound: if bound >= (1 - gap) * incumbent the incumbent is within the gap and
+ *          is the answer; else depth-first over the pairs in forward order, each pair's candidates
+ *          fastest first, a child skipped if it does not fit its points, a subtree entered only
+ *          if its bound < (1 - gap) * incumbent, a complete selection taken if strictly better.
+ *          At most `node_cap` children are visited (then the incumbent stands; reported).
  *   M4 score: the schedule re-timed (O7-O10) with every pair's selected latencies and
  *      activations.
  * ====================================================================================== */
@@ -1004,10 +1016,208 @@ int oracle_mem_candidates(uint32_t n_strat, const uint32_t *f, const uint32_t *b
     return (int)k;
 }
 
+/* ---------------- M3: the per-rank ILP ----------------
+ * n pairs in forward order; pair p is live at point k (the k-th forward slot, sF[k]) iff
+ * sF[p] <= sF[k] < sB[p]; cand[(p*Sst + c)*3 + {0,1,2}] = (F, B, mem) of candidate c < nc[p],
+ * sorted by memory ascending. cur[p] (out) = the selected candidate. stats (may be NULL):
+ * [0] warm-start objective, [1] root bound, [2] final objective, [3] B&B children visited,
+ * [4] flags: 1 = candidate 0 infeasible (nothing selected), 2 = the warm start was within the gap
+ * at the root, 4 = node_cap reached (oracle_memopt adds 8 = malformed record / n = 0, not solved).
+ * Returns 0. */
+typedef struct {
+    uint32_t n, Sst, gap_pm, node_cap;
+    const uint32_t *sF, *sB, *nc;
+    const uint64_t *cand;
+    int64_t M;
+    uint32_t *pick;      /* current partial selection (depth-first) */
+    uint32_t *best;      /* incumbent */
+    uint8_t *kstar;      /* M3b: the points whose constraint the bound keeps */
+    uint64_t inc, nodes;
+    int capped;
+} ilp_t;
+
+static uint64_t c_lat(const ilp_t *I, uint32_t p, uint32_t c) {
+    const uint64_t *a = I->cand + ((size_t)p * I->Sst + c) * 3;
+    return a[0] + a[1];
+}
+static uint64_t c_mem(const ilp_t *I, uint32_t p, uint32_t c) { return I->cand[((size_t)p * I->Sst + c) * 3 + 2]; }
+static int live_at(const ilp_t *I, uint32_t p, uint32_t k) { return I->sF[p] <= I->sF[k] && I->sF[k] < I->sB[p]; }
+
+/* memory at point k: pairs < nfix at their pick, the others at candidate 0 */
+static int64_t used_at(const ilp_t *I, uint32_t k, uint32_t nfix) {
+    int64_t u = 0;
+    for (uint32_t p = 0; p < I->n; p++)
+        if (live_at(I, p, k)) u += (int64_t)c_mem(I, p, p < nfix ? I->pick[p] : 0);
+    return u;
+}
+
+/* M3b: lower bound on sum lat with pairs < nfix fixed at their pick; UINT64_MAX if infeasible.
+ * Lagrangian relaxation of the memory constraints at the points K* (kstar[k] = 1) with one
+ * multiplier mu >= 0 (fixed point, mu = mu_int / 2^16): for ANY mu
+ *   L(mu) = sum_fixed lat + sum_free min_c (lat_c + mu * c_p * mem_c) - mu * R,
+ *   c_p = #{k in K*: p live at k},  R = sum_{k in K*} (M - memory of the fixed pairs live at k),
+ * is <= the ILP optimum (weak duality: every feasible selection has sum_free c_p mem_p <= R).
+ * mu is found by bisection on the sign of R - D(mu), D(mu) = sum_free c_p * mem of the pair's
+ * minimiser (ties: less memory); the bound is the ILP-integral ceil(L) at the better end. */
+#define ILP_SHIFT 16
+static void ilp_eval(const ilp_t *I, uint32_t nfix, const uint32_t *cp, uint64_t mu, uint64_t *D, unsigned __int128 *V) {
+    *D = 0; *V = 0;
+    for (uint32_t p = nfix; p < I->n; p++) {
+        unsigned __int128 best = 0;
+        uint64_t bm = 0;
+        for (uint32_t c = 0; c < I->nc[p]; c++) {
+            unsigned __int128 v = ((unsigned __int128)c_lat(I, p, c) << ILP_SHIFT) + (unsigned __int128)mu * cp[p] * c_mem(I, p, c);
+            if (c == 0 || v < best || (v == best && c_mem(I, p, c) < bm)) { best = v; bm = c_mem(I, p, c); }
+        }
+        *V += best;
+        *D += (uint64_t)cp[p] * bm;
+    }
+}
+
+static uint64_t ilp_L(const ilp_t *I, uint32_t nfix, const uint32_t *cp, uint64_t mu, int64_t R, uint64_t fixed) {
+    uint64_t D;
+    unsigned __int128 V;
+    ilp_eval(I, nfix, cp, mu, &D, &V);
+    unsigned __int128 take = (unsigned __int128)mu * (uint64_t)R;      /* R >= 0 when feasible */
+    if (V <= take) return fixed;
+    unsigned __int128 num = V - take;
+    uint64_t q = (uint64_t)(num >> ILP_SHIFT) + ((num & ((1u << ILP_SHIFT) - 1)) ? 1 : 0);   /* ceil */
+    return fixed + q;
+}
+
+static uint64_t ilp_bound(const ilp_t *I, uint32_t nfix) {
+    const uint32_t n = I->n;
+    for (uint32_t k = 0; k < n; k++)
+        if (used_at(I, k, nfix) > I->M) return UINT64_MAX;
+    uint64_t fixed = 0;
+    for (uint32_t p = 0; p < nfix; p++) fixed += c_lat(I, p, I->pick[p]);
+    uint32_t *cp = calloc(n + 1, sizeof(uint32_t));
+    int64_t R = 0;
+    for (uint32_t k = 0; k < n; k++) {
+        if (!I->kstar[k]) continue;
+        int64_t fx = 0;
+        for (uint32_t p = 0; p < n; p++)
+            if (live_at(I, p, k)) {
+                if (p < nfix) fx += (int64_t)c_mem(I, p, I->pick[p]);
+                else cp[p]++;
+            }
+        R += I->M - fx;
+    }
+    uint64_t D;
+    unsigned __int128 V;
+    uint64_t lo = 0, hi = 1, out;
+    ilp_eval(I, nfix, cp, 0, &D, &V);
+    if ((int64_t)D <= R) {
+        out = ilp_L(I, nfix, cp, 0, R, fixed);
+    } else {
+        for (int it = 0; it < 62; it++) {          /* D(hi) <= R: every pair at its least memory fits */
+            ilp_eval(I, nfix, cp, hi, &D, &V);
+            if ((int64_t)D <= R) break;
+            lo = hi;
+            hi *= 2;
+        }
+        while (hi - lo > 1) {
+            uint64_t mid = lo + (hi - lo) / 2;
+            ilp_eval(I, nfix, cp, mid, &D, &V);
+            if ((int64_t)D <= R) hi = mid; else lo = mid;
+        }
+        uint64_t a = ilp_L(I, nfix, cp, lo, R, fixed), b = ilp_L(I, nfix, cp, hi, R, fixed);
+        out = a > b ? a : b;
+    }
+    free(cp);
+    return out;
+}
+
+/* within the gap: 1000 * bound >= (1000 - gap) * incumbent */
+static int ilp_within(const ilp_t *I, uint64_t bound) {
+    return (unsigned __int128)bound * 1000u >= (unsigned __int128)I->inc * (1000u - I->gap_pm);
+}
+
+/* M3c: depth-first over pair d's candidates, fastest first */
+static void ilp_dfs(ilp_t *I, uint32_t d) {
+    for (int c = (int)I->nc[d] - 1; c >= 0; c--) {
+        if (I->nodes >= I->node_cap) { I->capped = 1; return; }
+        I->nodes++;
+        I->pick[d] = (uint32_t)c;
+        int fits = 1;
+        for (uint32_t k = 0; k < I->n && fits; k++)
+            if (live_at(I, d, k) && used_at(I, k, d + 1) > I->M) fits = 0;
+        if (!fits) continue;
+        if (d + 1 == I->n) {
+            uint64_t obj = 0;
+            for (uint32_t p = 0; p < I->n; p++) obj += c_lat(I, p, I->pick[p]);
+            if (obj < I->inc) { I->inc = obj; memcpy(I->best, I->pick, sizeof(uint32_t) * I->n); }
+            continue;
+        }
+        uint64_t lb = ilp_bound(I, d + 1);
+        if (lb != UINT64_MAX && !ilp_within(I, lb)) ilp_dfs(I, d + 1);
+        if (I->capped) return;
+    }
+}
+
+int oracle_select_rank(uint32_t n, const uint32_t *sF, const uint32_t *sB, const uint32_t *nc, const uint64_t *cand,
+                       uint32_t Sst, int64_t M, uint32_t gap_pm, uint32_t node_cap, uint32_t *cur, uint64_t *stats) {
+    uint64_t sv[5] = {0, 0, 0, 0, 0};
+    ilp_t I = {n, Sst, gap_pm > 1000 ? 1000 : gap_pm, node_cap, sF, sB, nc, cand, M, NULL, NULL, NULL, 0, 0, 0};
+    I.pick = calloc(n + 1, sizeof(uint32_t));
+    I.best = calloc(n + 1, sizeof(uint32_t));
+    I.kstar = calloc(n + 1, 1);
+    for (uint32_t p = 0; p < n; p++) cur[p] = 0;
+    /* M3a: the greedy warm start */
+    int64_t *slack = malloc(sizeof(int64_t) * (n + 1));
+    int feasible = 1;
+    for (uint32_t k = 0; k < n; k++) {
+        slack[k] = M - used_at(&I, k, 0);
+        if (slack[k] < 0) feasible = 0;
+    }
+    while (feasible) {
+        int best = -1;
+        uint64_t bl = 0, bm = 1;
+        for (uint32_t p = 0; p < n; p++) {
+            if (cur[p] + 1 >= nc[p]) continue;
+            uint64_t dl = c_lat(&I, p, cur[p]) - c_lat(&I, p, cur[p] + 1), dm = c_mem(&I, p, cur[p] + 1) - c_mem(&I, p, cur[p]);
+            int ok = 1;
+            for (uint32_t k = 0; k < n && ok; k++)
+                if (live_at(&I, p, k) && slack[k] < (int64_t)dm) ok = 0;
+            if (!ok) continue;
+            /* dl/dm > bl/bm, exactly; ties keep the earlier forward slot (lower p) */
+            if (best < 0 || (unsigned __int128)dl * bm > (unsigned __int128)bl * dm) { best = (int)p; bl = dl; bm = dm; }
+        }
+        if (best < 0) break;
+        for (uint32_t k = 0; k < n; k++)
+            if (live_at(&I, (uint32_t)best, k)) slack[k] -= (int64_t)bm;
+        cur[best]++;
+    }
+    /* K*: the points where the warm start blocks a pair (its next step does not fit there) */
+    for (uint32_t k = 0; k < n && feasible; k++)
+        for (uint32_t p = 0; p < n; p++)
+            if (live_at(&I, p, k) && cur[p] + 1 < nc[p] && slack[k] < (int64_t)(c_mem(&I, p, cur[p] + 1) - c_mem(&I, p, cur[p])))
+                I.kstar[k] = 1;
+    free(slack);
+    if (!feasible) {
+        sv[4] = 1;
+    } else {
+        for (uint32_t p = 0; p < n; p++) { I.inc += c_lat(&I, p, cur[p]); I.best[p] = cur[p]; }
+        sv[0] = I.inc;
+        /* M3b at the root, M3c if the warm start is not provably within the gap */
+        uint64_t lb = ilp_bound(&I, 0);
+        sv[1] = lb;
+        if (ilp_within(&I, lb)) sv[4] |= 2;
+        else if (n > 0) ilp_dfs(&I, 0);
+        if (I.capped) sv[4] |= 4;
+        for (uint32_t p = 0; p < n; p++) cur[p] = I.best[p];
+        sv[2] = I.inc;
+        sv[3] = I.nodes;
+    }
+    if (stats) memcpy(stats, sv, sizeof(sv));
+    free(I.pick); free(I.best); free(I.kstar);
+    return 0;
+}
+
 /* M2-M4 for candidate x: sel [P][2][n_max] (candidate index of the pair at forward position p /
  * backward position q), then the re-timed result. */
 static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, uint64_t x, uint8_t *sel,
-                       ores *res, uint64_t *peaks) {
+                       ores *res, uint64_t *peaks, uint64_t *rstats /* [P][5] or NULL */) {
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m, n_max = cs->n_max, fbw = cs->fbw;
     const uint8_t *split = cs->split + x * (uint64_t)m * nm;
     const uint16_t *fwd = cs->fwd + x * (uint64_t)n_max, *bwd = cs->bwd + x * (uint64_t)n_max;
@@ -1016,7 +1226,11 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
     memset(sel, 0, (size_t)P * 2 * n_max);
     ores r0;
     eval_one(pb, cs, x, &r0, NULL, NULL, NULL, NULL);             /* encoding checks (O4) */
-    if (r0.status == ST_BAD || n == 0) { eval_one(pb, cs, x, res, peaks, NULL, NULL, NULL); return; }
+    if (r0.status == ST_BAD || n == 0) {
+        if (rstats) for (uint32_t r = 0; r < P; r++) { memset(rstats + 5 * (size_t)r, 0, 5 * sizeof(uint64_t)); rstats[5 * (size_t)r + 4] = 8; }
+        eval_one(pb, cs, x, res, peaks, NULL, NULL, NULL);
+        return;
+    }
     uint32_t idmax = seg_count_max(pb);
     uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
     uint32_t *W = calloc(idmax + 1, sizeof(uint32_t)), *si = calloc(idmax + 1, sizeof(uint32_t)), *sk = calloc(idmax + 1, sizeof(uint32_t));
@@ -1039,15 +1253,13 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
     uint64_t *cl = malloc(sizeof(uint64_t) * 3 * mn->S * n);     /* candidates of each pair */
     uint32_t *nc = malloc(sizeof(uint32_t) * n), *cur = malloc(sizeof(uint32_t) * n);
     uint32_t *sF = malloc(sizeof(uint32_t) * n), *sB = malloc(sizeof(uint32_t) * n), *qpos = malloc(sizeof(uint32_t) * n);
-    int64_t *slack = malloc(sizeof(int64_t) * 2 * n);
-    uint32_t *fsl = malloc(sizeof(uint32_t) * n);                /* forward slots = the points s_k */
     for (uint32_t r = 0; r < P; r++) {
         /* the rank's order: slot of the p-th forward and of the q-th backward stage (O5) */
         uint32_t fi = 0, bi = 0;
         uint32_t *slotB_of_seg = malloc(sizeof(uint32_t) * (idmax + 1)), *qpos_of_seg = malloc(sizeof(uint32_t) * (idmax + 1));
         for (uint32_t t = 0; t < 2 * n; t++) {
             if ((fb[r * fbw + t / 32] >> (t % 32)) & 1u) { slotB_of_seg[bwd[bi]] = t; qpos_of_seg[bwd[bi]] = bi; bi++; }
-            else { sF[fi] = t; fsl[fi] = t; fi++; }
+            else { sF[fi] = t; fi++; }
         }
         for (uint32_t p = 0; p < n; p++) {                          /* pair p = segment fwd[p] */
             uint32_t s = fwd[p], i = si[s], lay = layers_of(pb, i, sk[s] * P + r), toff = pb->tab_off[i] + W[s];
@@ -1061,34 +1273,9 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
             sB[p] = slotB_of_seg[s];
             qpos[p] = qpos_of_seg[s];
         }
-        /* M3: slack at every forward slot with candidate 0 everywhere */
-        int feasible = 1;
-        for (uint32_t k = 0; k < n; k++) {
-            int64_t used = 0;
-            for (uint32_t p = 0; p < n; p++)
-                if (sF[p] <= fsl[k] && fsl[k] < sB[p]) used += (int64_t)cl[(size_t)3 * mn->S * p + 2];
-            slack[k] = (int64_t)pb->budget_kib[r] - used;
-            if (slack[k] < 0) feasible = 0;
-        }
-        while (feasible) {
-            int best = -1;
-            uint64_t bl = 0, bm = 1;
-            for (uint32_t p = 0; p < n; p++) {
-                if (cur[p] + 1 >= nc[p]) continue;
-                const uint64_t *a = cl + (size_t)3 * mn->S * p + 3 * cur[p];
-                uint64_t dl = (a[0] + a[1]) - (a[3] + a[4]), dm = a[5] - a[2];
-                int ok = 1;
-                for (uint32_t k = 0; k < n && ok; k++)
-                    if (sF[p] <= fsl[k] && fsl[k] < sB[p] && slack[k] < (int64_t)dm) ok = 0;
-                if (!ok) continue;
-                /* dl/dm > bl/bm, exactly; ties keep the earlier forward slot (lower p) */
-                if (best < 0 || (unsigned __int128)dl * bm > (unsigned __int128)bl * dm) { best = (int)p; bl = dl; bm = dm; }
-            }
-            if (best < 0) break;
-            for (uint32_t k = 0; k < n; k++)
-                if (sF[best] <= fsl[k] && fsl[k] < sB[best]) slack[k] -= (int64_t)bm;
-            cur[best]++;
-        }
+        /* M3: the rank's ILP */
+        oracle_select_rank(n, sF, sB, nc, cl, mn->S, (int64_t)pb->budget_kib[r], mn->gap_pm, mn->node_cap, cur,
+                           rstats ? rstats + 5 * (size_t)r : NULL);
         for (uint32_t p = 0; p < n; p++) {
             const uint64_t *a = cl + (size_t)3 * mn->S * p + 3 * cur[p];
             uint64_t *o = ovr + ((uint64_t)r * (idmax + 1) + fwd[p]) * 3;
@@ -1100,7 +1287,7 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
     }
     eval_one(pb, cs, x, res, peaks, NULL, NULL, ovr);          /* M4 */
     free(base); free(W); free(si); free(sk); free(ovr); free(cl); free(nc); free(cur);
-    free(sF); free(sB); free(qpos); free(slack); free(fsl);
+    free(sF); free(sB); free(qpos);
 }
 
 typedef struct {
@@ -1109,7 +1296,7 @@ typedef struct {
     const ocands *cs;
     uint64_t lo, hi, first;
     uint8_t *sel;
-    uint64_t *makespan, *busy, *peaks;
+    uint64_t *makespan, *busy, *peaks, *rstats;
     uint32_t *status, *oom;
     double *bubble;
 } mjob_t;
@@ -1120,7 +1307,8 @@ static void *mworker(void *arg) {
     for (uint64_t x = j->lo; x < j->hi; x++) {
         ores r;
         uint64_t o = x - j->first;
-        memopt_one(j->pb, j->mn, j->cs, x, j->sel + o * (uint64_t)P * 2 * j->cs->n_max, &r, j->peaks ? j->peaks + o * P : NULL);
+        memopt_one(j->pb, j->mn, j->cs, x, j->sel + o * (uint64_t)P * 2 * j->cs->n_max, &r, j->peaks ? j->peaks + o * P : NULL,
+                   j->rstats ? j->rstats + o * 5 * P : NULL);
         j->makespan[o] = r.makespan; j->busy[o] = r.busy; j->status[o] = r.status;
         j->oom[o] = r.oom_mask; j->bubble[o] = r.bubble;
     }
@@ -1130,9 +1318,10 @@ static void *mworker(void *arg) {
 int oracle_memopt(const oproblem *pb, uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma,
                   uint32_t S, const ocands *cs, uint64_t first, uint64_t count, uint8_t *sel /* [count][P][2][n_max] */,
                   uint64_t *makespan, uint32_t *status, uint32_t *oom_mask, double *bubble, uint64_t *peaks,
-                  uint64_t *busy, int threads) {
+                  uint64_t *busy, int threads, uint32_t gap_pm, uint32_t node_cap,
+                  uint64_t *rank_stats /* [count][P][5] (oracle_select_rank's stats) or NULL */) {
     if (n_strat == 0 || n_strat > 8 || S < 2 || S > 16) return -1;
-    omenu mn = {n_strat, S, mf, mb, ma};
+    omenu mn = {n_strat, S, mf, mb, ma, gap_pm, node_cap};
     if (threads < 1) threads = 1;
     if (threads > 512) threads = 512;
     if ((uint64_t)threads > count) threads = count ? (int)count : 1;
@@ -1143,7 +1332,7 @@ int oracle_memopt(const oproblem *pb, uint32_t n_strat, const uint32_t *mf, cons
         uint64_t lo = first + per * t, hi = lo + per;
         if (hi > first + count) hi = first + count;
         if (lo > hi) lo = hi;
-        jobs[t] = (mjob_t){pb, &mn, cs, lo, hi, first, sel, makespan, busy, peaks, status, oom_mask, bubble};
+        jobs[t] = (mjob_t){pb, &mn, cs, lo, hi, first, sel, makespan, busy, peaks, rank_stats, status, oom_mask, bubble};
         pthread_create(&th[t], NULL, mworker, &jobs[t]);
     }
     for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
