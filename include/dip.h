@@ -198,15 +198,30 @@ dip_status dip_strategy_candidates(const dip_model *m, uint32_t module, uint32_t
                                    uint64_t *out, uint32_t *count);
 
 /* Per-rank strategy selection and re-timing of `count` device records (R-39, R-40):
- * for every (record, rank) the pairs start at candidate 0 and the greedy warm start moves
- * the pair with the largest latency saving per KiB up while every forward slot it covers stays
- * within the rank's budget; then the schedules are scored with the selected latencies and
- * activations (results / peaks / fused argmin key as dip_eval_schedules). d_sel: device
+ * for every (record, rank) the per-rank ILP of P:572-582 (minimise the summed pair latency subject
+ * to the rank's budget at every forward slot) is solved to the relative optimality gap set by
+ * dip_set_memopt_solver (default 5 %): the pairs start at candidate 0, the greedy warm
+ * start moves the pair with the largest latency saving per KiB up while every forward slot
+ * it covers stays within the budget; a Lagrangian bound (R-39) certifies it, else a
+ * depth-first branch and bound improves it (at most node_cap children per rank). Then the schedules
+ * are scored with the selected latencies and activations (results / peaks / fused argmin key as
+ * dip_eval_schedules). d_sel: device
  * [count][P][2][n_max] u8 out -- sel[c][r][0][p] = candidate of the pair whose forward is the
  * p-th forward stage, sel[c][r][1][q] = the same for the q-th backward stage (zero beyond n;
  * unspecified for BAD_ENCODING records). Two launches on `stream`, asynchronous. */
 dip_status dip_memopt(const dip_model *m, dip_workspace *w, const void *d_records, size_t count, uint8_t *d_sel,
                       dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+
+/* The per-rank ILP solver's settings for dip_memopt: relative optimality gap in per mille
+ * (default 50 = the paper's 5 %, 0 = exact) and the branch-and-bound child budget per (record, rank)
+ * (default 4096; when it is reached the incumbent stands and dip_memopt_stats counts it).
+ * DIP_EINVAL if gap_permille > 1000 or node_cap == 0. */
+dip_status dip_set_memopt_solver(dip_model *m, uint32_t gap_permille, uint32_t node_cap);
+
+/* Counters of the last dip_memopt on `w`, out[5] host: (record, rank) instances solved, certified
+ * at the root (the warm start within the gap), searched by branch and bound, stopped by node_cap,
+ * and the branch-and-bound children visited in total. Synchronous on `stream`. */
+dip_status dip_memopt_stats(const dip_workspace *w, uint64_t *out, void *stream);
 
 /* DIP's MCTS segment reordering (§5.1) with batched
  * GPU rollouts. For the given split, classes = (direction, microbatch, module, chunk k) with M > 0

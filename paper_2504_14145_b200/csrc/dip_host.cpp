@@ -39,6 +39,10 @@ static void fill_shape(dip_model *M) {
     kp.nsplit = M->nsplit;
     kp.warps_per_block = M->wpb;
     kp.cpg = M->cpg;
+    if (!kp.node_cap) {            // f3 solver defaults (dip_set_memopt_solver): 5 % gap
+        kp.gap_pm = 50;
+        kp.node_cap = 4096;
+    }
 }
 
 extern "C" {

@@ -44,6 +44,8 @@ struct KParams {
     const int32_t *crow;        // f3: per chunk row, ctab base of its (module, layers) type - tab_off * S
     const uint16_t *srank;      // f3: per ctab entry c, the rank of the step c -> c+1 by saving per KiB
     uint32_t S;                 // f3: candidates per (type, W)
+    uint32_t gap_pm, node_cap;  // f3: the per-rank ILP's optimality gap (per mille) and B&B child budget
+    unsigned long long *mo_stats;   // f3: [5] solved, certified at the root, searched, capped, B&B children
     uint64_t count, index_base;
     dip_result *results;
     uint32_t *peaks;

@@ -42,6 +42,94 @@ __device__ __forceinline__ bool mc_before(const MC &a, const MC &b, bool by_mem)
     return a.f < b.f;
 }
 
+// ---- M3b / M3c helpers (one warp per (schedule, rank); all control is warp-uniform)
+__device__ __forceinline__ unsigned __int128 warp_sum_u128(unsigned __int128 v) {
+    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        const unsigned long long s = lo + lo2;
+        hi = hi + hi2 + (s < lo ? 1ull : 0ull);
+        lo = s;
+    }
+    return ((unsigned __int128)hi << 64) | lo;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int ILP_SHIFT = 16;   // mu = mu_int / 2^16 (the oracle's fixed point)
+
+// D(mu) = sum over free pairs p >= nfix of c_p * memory of argmin_c (lat_c * 2^16 + mu * c_p * mem_c)
+// (ties: the earlier = smaller-memory candidate), V(mu) = sum of the minima; warp-summed, exact
+__device__ __forceinline__ void ilp_eval(const uint4 *__restrict__ ctab, const uint16_t *cbr, const uint8_t *cn,
+                                         const uint32_t *cpa, uint32_t S, uint32_t n, uint32_t nfix,
+                                         unsigned long long mu, bool wantV, unsigned long long *D,
+                                         unsigned __int128 *V) {
+    unsigned long long d = 0;
+    unsigned __int128 v = 0;
+    for (uint32_t p = nfix + (threadIdx.x & 31); p < n; p += 32) {
+        const uint32_t cb = (uint32_t)cbr[p] * S, cnt = (cn[p] >> 4) + 1u;
+        const unsigned long long cp = cpa[p];
+        unsigned __int128 best = 0;
+        unsigned long long bm = 0;
+        for (uint32_t c = 0; c < cnt; c++) {
+            const uint4 E = __ldg(&ctab[cb + c]);
+            const unsigned __int128 x = ((unsigned __int128)((unsigned long long)E.x + E.y) << ILP_SHIFT) +
+                                        (unsigned __int128)mu * (cp * E.z);
+            if (c == 0 || x < best) { best = x; bm = E.z; }
+        }
+        d += cp * bm;
+        v += best;
+    }
+    *D = warp_sum_u64(d);
+    if (wantV) *V = warp_sum_u128(v);
+}
+
+__device__ __forceinline__ unsigned long long ilp_L(const uint4 *__restrict__ ctab, const uint16_t *cbr, const uint8_t *cn,
+                                                    const uint32_t *cpa, uint32_t S, uint32_t n, uint32_t nfix,
+                                                    unsigned long long mu, long long R, unsigned long long fixed) {
+    unsigned long long D;
+    unsigned __int128 V;
+    ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, mu, true, &D, &V);
+    const unsigned __int128 take = (unsigned __int128)mu * (unsigned long long)R;
+    if (V <= take) return fixed;
+    const unsigned __int128 num = V - take;
+    return fixed + (unsigned long long)(num >> ILP_SHIFT) + ((num & ((1u << ILP_SHIFT) - 1)) ? 1ull : 0ull);
+}
+
+// M3b: the Lagrangian bound with pairs < nfix fixed (their latency summed in `fixed`, their memory
+// taken out of R = sum over K* of (budget - fixed memory live there)); bisection on mu exactly as
+// the oracle's (same integer sequence, so the same bound)
+__device__ unsigned long long ilp_bound(const uint4 *__restrict__ ctab, const uint16_t *cbr, const uint8_t *cn,
+                                        const uint32_t *cpa, uint32_t S, uint32_t n, uint32_t nfix, long long R,
+                                        unsigned long long fixed) {
+    unsigned long long D;
+    unsigned __int128 V;
+    ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, 0ull, false, &D, &V);
+    if ((long long)D <= R) return ilp_L(ctab, cbr, cn, cpa, S, n, nfix, 0ull, R, fixed);
+    unsigned long long lo = 0, hi = 1;
+    for (int it = 0; it < 62; it++) {
+        ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, hi, false, &D, &V);
+        if ((long long)D <= R) break;
+        lo = hi;
+        hi *= 2;
+    }
+    while (hi - lo > 1) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, mid, false, &D, &V);
+        if ((long long)D <= R) hi = mid; else lo = mid;
+    }
+    const unsigned long long a = ilp_L(ctab, cbr, cn, cpa, S, n, nfix, lo, R, fixed);
+    const unsigned long long b = ilp_L(ctab, cbr, cn, cpa, S, n, nfix, hi, R, fixed);
+    return a > b ? a : b;
+}
+
+__device__ __forceinline__ bool ilp_within(unsigned long long bound, unsigned long long inc, uint32_t gap_pm) {
+    return (unsigned __int128)bound * 1000u >= (unsigned __int128)inc * (1000u - gap_pm);
+}
+
 }  // namespace
 
 constexpr int MAX_S = 16;
@@ -343,6 +431,141 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                     dms[a0] = dm;
                 }
                 __syncwarp();
+            }
+        }
+        if (feasible) {
+            // ---- M3b / M3c: is the warm start provably within the gap? else branch and bound
+            const uint4 *__restrict__ ctab = kp.ctab;
+            // K*: the points where the warm start blocks a pair (dms[p] = its next step's KiB, 0 = none)
+            for (uint32_t k = lane; k < n; k += 32) key[k] = 0;
+            __syncwarp();
+            for (uint32_t p = lane; p < n; p += 32) {
+                const uint32_t dm = dms[p], e = eP[p];
+                if (!dm) continue;
+                for (uint32_t k = p; k < e; k++)
+                    if ((int64_t)slack[k] < (int64_t)dm) key[k] = 1u;
+            }
+            __syncwarp();
+            uint32_t nK = 0;
+            for (uint32_t k0 = 0; k0 < n; k0 += 32) {       // inclusive prefix count of K* in key[]
+                const uint32_t k = k0 + lane;
+                uint32_t v = k < n ? key[k] : 0u;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(FULL, v, o);
+                    if (lane >= o) v += u;
+                }
+                if (k < n) key[k] = nK + v;
+                nK += __shfl_sync(FULL, v, 31);
+            }
+            __syncwarp();
+            // c_p = K* points in pair p's range (into dms[], dead now); the warm start's objective
+            unsigned long long inc = 0;
+            for (uint32_t p = lane; p < n; p += 32) {
+                const uint32_t e = eP[p];
+                dms[p] = e > p ? key[e - 1] - (p ? key[p - 1] : 0u) : 0u;
+                const uint4 E = __ldg(&ctab[(uint32_t)cbr[p] * S + (cn[p] & 15u)]);
+                inc += (unsigned long long)E.x + E.y;
+            }
+            inc = warp_sum_u64(inc);
+            __syncwarp();
+            const uint32_t *cpa = dms;
+            const long long Mk = (long long)nK * (long long)bud;
+            const unsigned long long lb0 = ilp_bound(ctab, cbr, cn, cpa, S, n, 0, Mk, 0ull);
+            const bool certified = ilp_within(lb0, inc, kp.gap_pm);
+            unsigned long long nodes = 0;
+            bool capped = false;
+            if (!certified) {
+                // branch and bound (the oracle's depth-first order): candidate-0 slack profile again
+                for (uint32_t k = lane; k < n; k += 32) slack[k] = 0;
+                __syncwarp();
+                for (uint32_t p = lane; p < n; p += 32) {
+                    const uint32_t e = eP[p];
+                    if (e > p) {
+                        const int32_t z = (int32_t)__ldg(&ctab[(uint32_t)cbr[p] * S]).z;
+                        atomicAdd(&slack[p], z);
+                        if (e < n) atomicSub(&slack[e], z);
+                    }
+                }
+                __syncwarp();
+                {
+                    int32_t run = 0;
+                    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+                        const uint32_t k = k0 + lane;
+                        int32_t v = k < n ? slack[k] : 0;
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int32_t u = __shfl_up_sync(FULL, v, o);
+                            if (lane >= o) v += u;
+                        }
+                        if (k < n) slack[k] = bud - (run + v);
+                        run += __shfl_sync(FULL, v, 31);
+                    }
+                }
+                uint8_t *dpick = reinterpret_cast<uint8_t *>(key);   // key[] is dead: picks and
+                uint8_t *tryc = dpick + n_max;                          // next-candidate-to-try + 1
+                if (lane == 0) tryc[0] = (uint8_t)((cn[0] >> 4) + 1u);
+                __syncwarp();
+                uint32_t d = 0;
+                unsigned long long fixed = 0;
+                long long rfix = 0;
+                for (;;) {
+                    const uint32_t t = tryc[d];
+                    if (t == 0) {                                    // exhausted: back to d - 1
+                        if (d == 0) break;
+                        d--;
+                        const uint32_t c = dpick[d], cb = (uint32_t)cbr[d] * S;
+                        const uint4 E = __ldg(&ctab[cb + c]);
+                        const int32_t dm = (int32_t)(E.z - __ldg(&ctab[cb]).z);
+                        for (uint32_t k = d + lane; k < (uint32_t)eP[d]; k += 32) slack[k] += dm;
+                        fixed -= (unsigned long long)E.x + E.y;
+                        rfix -= (long long)cpa[d] * E.z;
+                        __syncwarp();
+                        continue;
+                    }
+                    if (nodes >= kp.node_cap) { capped = true; break; }
+                    nodes++;
+                    const uint32_t c = t - 1u, cb = (uint32_t)cbr[d] * S, e = eP[d];
+                    __syncwarp();
+                    if (lane == 0) tryc[d] = (uint8_t)c;
+                    const uint4 E = __ldg(&ctab[cb + c]);
+                    const int32_t dm = (int32_t)(E.z - __ldg(&ctab[cb]).z);
+                    int32_t mn = INF;
+                    for (uint32_t k = d + lane; k < e; k += 32) mn = min(mn, slack[k]);
+                    mn = __reduce_min_sync(FULL, mn);
+                    if ((int64_t)mn < (int64_t)dm) { __syncwarp(); continue; }      // does not fit
+                    __syncwarp();
+                    for (uint32_t k = d + lane; k < e; k += 32) slack[k] -= dm;
+                    if (lane == 0) dpick[d] = (uint8_t)c;
+                    fixed += (unsigned long long)E.x + E.y;
+                    rfix += (long long)cpa[d] * E.z;
+                    __syncwarp();
+                    bool descend = false;
+                    if (d + 1 == n) {                                 // a complete selection
+                        if (fixed < inc) {
+                            inc = fixed;
+                            for (uint32_t p = lane; p < n; p += 32) cn[p] = (uint8_t)((cn[p] & 0xF0u) | dpick[p]);
+                        }
+                    } else {
+                        const unsigned long long lb = ilp_bound(ctab, cbr, cn, cpa, S, n, d + 1, Mk - rfix, fixed);
+                        descend = !ilp_within(lb, inc, kp.gap_pm);
+                    }
+                    __syncwarp();
+                    if (descend) {
+                        d++;
+                        if (lane == 0) tryc[d] = (uint8_t)((cn[d] >> 4) + 1u);
+                        __syncwarp();
+                        continue;
+                    }
+                    for (uint32_t k = d + lane; k < e; k += 32) slack[k] += dm;   // undo the pick
+                    fixed -= (unsigned long long)E.x + E.y;
+                    rfix -= (long long)cpa[d] * E.z;
+                    __syncwarp();
+                }
+            }
+            if (lane == 0 && kp.mo_stats && n > 0) {
+                atomicAdd(kp.mo_stats + 0, 1ull);
+                atomicAdd(kp.mo_stats + (certified ? 1 : 2), 1ull);
+                if (capped) atomicAdd(kp.mo_stats + 3, 1ull);
+                if (nodes) atomicAdd(kp.mo_stats + 4, nodes);
             }
         }
         // the backward row needs each pair's backward position again: rebuild the segment -> position

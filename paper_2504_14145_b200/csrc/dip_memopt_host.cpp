@@ -218,9 +218,27 @@ extern "C" dip_status dip_memopt(const dip_model *M, dip_workspace *w, const voi
     kp.records = static_cast<const uint8_t *>(d_records);
     kp.count = count;
     kp.counter = w->d_misc + 5;
+    kp.mo_stats = w->d_misc + 10;
     CUDA_TRY(cudaMemsetAsync(w->d_misc + 5, 0, sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 10, 0, 5 * sizeof(unsigned long long), s));
     const uint64_t warps = std::min<uint64_t>((uint64_t)M->mo_grid * 4, count * M->P);
     CUDA_TRY(dipk::launch_memopt(kp, d_sel, M->mo_warp_bytes, (int)((warps + 3) / 4), s));
     g_launches++;
     return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s, nullptr, d_sel);
+}
+
+extern "C" dip_status dip_set_memopt_solver(dip_model *M, uint32_t gap_permille, uint32_t node_cap) {
+    if (!M) return fail(DIP_EINVAL, "null model");
+    if (gap_permille > 1000 || node_cap == 0) return fail(DIP_EINVAL, "gap_permille must be <= 1000, node_cap > 0");
+    M->kp.gap_pm = gap_permille;
+    M->kp.node_cap = node_cap;
+    return DIP_OK;
+}
+
+extern "C" dip_status dip_memopt_stats(const dip_workspace *w, uint64_t *out, void *stream) {
+    if (!w || !out) return fail(DIP_EINVAL, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemcpyAsync(out, w->d_misc + 10, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return DIP_OK;
 }

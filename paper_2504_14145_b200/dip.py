@@ -119,6 +119,8 @@ def lib():
     L.dip_strategy_candidates.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp,
                                           ctypes.POINTER(ctypes.c_uint32)]
     L.dip_memopt.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    L.dip_set_memopt_solver.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32]
+    L.dip_memopt_stats.argtypes = [vp, vp, vp]
     L.dip_comm_unique_id.argtypes = [vp]
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
@@ -128,7 +130,8 @@ def lib():
               "dip_eval_host",
               "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key",
               "dip_timeline", "dip_compile_plan", "dip_validate_plan",
-              "dip_set_strategies", "dip_strategy_candidates", "dip_memopt"):
+              "dip_set_strategies", "dip_strategy_candidates", "dip_memopt", "dip_set_memopt_solver",
+              "dip_memopt_stats"):
         getattr(L, f).restype = st
     L.dip_launch_count.restype = ctypes.c_uint64
     L.dip_launch_count.argtypes = []
@@ -314,6 +317,19 @@ def memopt(model: Model, ws: Workspace, d_records, count: int, d_sel, d_results,
     re-timed scores (results as eval_schedules)."""
     _check(lib().dip_memopt(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_sel), _ptr(d_results),
                             _ptr(d_peaks), _stream(stream)), "dip_memopt")
+
+
+def set_memopt_solver(model: Model, gap_permille: int = 50, node_cap: int = 4096):
+    """f3: the per-rank ILP's relative optimality gap (per mille) and B&B child budget."""
+    _check(lib().dip_set_memopt_solver(model.handle, gap_permille, node_cap), "dip_set_memopt_solver")
+
+
+def memopt_stats(ws: Workspace, stream=None) -> dict:
+    """counters of the last memopt on ws: solved, certified (warm start within the gap at the root),
+    searched (branch and bound), capped (node_cap reached), nodes (B&B children in total)"""
+    out = np.zeros(5, np.uint64)
+    _check(lib().dip_memopt_stats(ws.handle, out.ctypes.data, _stream(stream)), "dip_memopt_stats")
+    return dict(zip(("solved", "certified", "searched", "capped", "nodes"), (int(v) for v in out)))
 
 
 def search(model: Model, ws: Workspace, split, seed: int, rounds: int, leaves: int, rollouts: int,

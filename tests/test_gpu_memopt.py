@@ -43,9 +43,10 @@ def test_candidate_table_parity(name, S):
             assert m.strategy_candidates(i, lay, W) == ref, (i, lay, W)
 
 
-def run(pb, cs, S=10):
+def run(pb, cs, S=10, menu=None, gap_pm=50, node_cap=4096, stats=None):
     m = dip.Model(pb, 0)
-    m.set_strategies(strategy_menu(pb), S)
+    m.set_strategies(strategy_menu(pb) if menu is None else menu, S)
+    dip.set_memopt_solver(m, gap_pm, node_cap)
     ws = dip.Workspace(m)
     s = torch.cuda.current_stream()
     d_rec = torch.from_numpy(m.encode(cs)).cuda()
@@ -56,13 +57,28 @@ def run(pb, cs, S=10):
     win = dip.argmin(m, ws, cs.count, stream=s)
     torch.cuda.synchronize()
     res = dip.results_view(d_res.cpu().numpy()).copy()
+    if stats is not None:
+        stats.update(dip.memopt_stats(ws, stream=s))
     return res, d_pk.cpu().numpy().view(np.uint32).copy(), d_sel.cpu().numpy().reshape(cs.count, pb.P, 2, pb.n_max), win
 
 
-def check(pb, cs, S=10, idx=None):
-    res, pk, sel, win = run(pb, cs, S)
+def check(pb, cs, S=10, idx=None, menu=None, gap_pm=50, node_cap=4096):
+    """GPU selections, re-timed results and solver counters == the oracle's (M1-M4)"""
+    menu = strategy_menu(pb) if menu is None else menu
+    gst = {}
+    res, pk, sel, win = run(pb, cs, S, menu, gap_pm, node_cap, gst)
     sub = cs if idx is None else cs.subset(idx)
-    rsel, ref = oracle.memopt(pb, sub, strategy_menu(pb), S=S, threads=16)
+    rsel, ref, rst = oracle.memopt(pb, sub, menu, S=S, threads=16, gap_pm=gap_pm, node_cap=node_cap, stats=True)
+    if idx is None and not (ref.status == oracle.ST_BAD).any():
+        # the solver's counters over every (record, rank) with n > 0 and a feasible candidate 0 (the
+        # selection kernel checks only the record's necessary conditions, so a malformed record the
+        # scorer rejects may still be counted there: compared on batches without such records)
+        fl = rst[:, :, 4].astype(np.int64)
+        solved = (fl & 9) == 0
+        want = {"solved": int(solved.sum()), "certified": int((solved & ((fl & 2) > 0)).sum()),
+                "searched": int((solved & ((fl & 2) == 0)).sum()), "capped": int(((fl & 4) > 0).sum()),
+                "nodes": int(rst[:, :, 3].sum())}
+        assert gst == want, (gst, want)
     if idx is not None:
         res, pk, sel = res[idx], pk[idx], sel[idx]
     assert np.array_equal(res["status"], ref.status), np.nonzero(res["status"] != ref.status)[0][:8]
@@ -95,11 +111,43 @@ def test_memopt_parity_other_S(S):
 
 
 def test_memopt_bench_size_sampled():
-    # the bench's f3 launch shape: 16,384 94B schedules in one call, 12 sampled against the oracle
+    # the bench's f3 launch shape: 16,384 94B schedules in one call, 256 sampled against the oracle
     pb = gen.make_problem("94B")
     cs = gen.generate(pb, 0, 16384, threads=16)
-    idx = [0, 1, 2, 777, 4095, 4096, 8191, 9000, 12345, 16000, 16382, 16383]
+    idx = np.unique(np.concatenate([[0, 1, 2, 4095, 4096, 8191, 16382, 16383],
+                                    np.random.default_rng(5).choice(16384, 248, replace=False)]))
     check(pb, cs, idx=idx)
+
+
+def _tiny(rng):
+    from tests.test_oracle_memopt import _tiny_instance
+    pb, menu, cs = _tiny_instance(rng)
+    pk0 = [int(v) for v in oracle.evaluate(pb, cs).peaks[0]]
+    pb.budget_kib = np.array([int(v * rng.uniform(1.0, 2.2)) for v in pk0], np.uint32)
+    return pb, menu, cs
+
+
+@pytest.mark.parametrize("gap_pm", [50, 0])
+def test_memopt_branch_and_bound_tiny(gap_pm):
+    """the ILP solver's branch and bound (M3c) on the tiny schedules of the oracle's brute-force pins:
+    identical selections, scores and solver counters (children visited included)"""
+    rng = np.random.default_rng(7)
+    searched = 0
+    for trial in range(40):
+        pb, menu, cs = _tiny(rng)
+        check(pb, cs, S=3, menu=menu, gap_pm=gap_pm)
+        st = {}
+        run(pb, cs, 3, menu, gap_pm, 4096, st)
+        searched += st["searched"]
+    assert searched > 0
+
+
+def test_memopt_branch_and_bound_full_size():
+    """exact solving (gap 0) at 12B size runs the depth-first search into its child budget: the GPU
+    must walk the oracle's tree node for node (same incumbent, same child count, same stops)"""
+    pb = gen.make_problem("12B")
+    cs = gen.generate(pb, 0, 6, p_mutate=0, p_bad=0)
+    check(pb, cs, gap_pm=0, node_cap=200)
 
 
 def test_strategy_menu_guards():
