@@ -43,7 +43,7 @@ class _OProblem(ctypes.Structure):
 
 class _OCands(ctypes.Structure):
     _fields_ = [("n_max", ctypes.c_uint32), ("fbw", ctypes.c_uint32)] + \
-        [(k, ctypes.c_void_p) for k in ("split", "n", "fwd", "bwd", "fb")]
+        [(k, ctypes.c_void_p) for k in ("split", "n", "fwd", "bwd", "fb", "ord")]
 
 
 def _load():
@@ -79,6 +79,9 @@ def _load():
         lib.oracle_memopt.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32] + [ctypes.c_void_p] * 3 + \
             [ctypes.c_uint32, ctypes.POINTER(_OCands), ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 7 + \
             [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
+        lib.oracle_mcts_table.restype = ctypes.c_uint32
+        lib.oracle_mcts_table.argtypes = [ctypes.c_uint32, ctypes.c_uint64] + [ctypes.c_uint32] * 3 + \
+            [ctypes.c_double] * 2 + [ctypes.c_void_p] * 7
         lib.oracle_select_rank.restype = ctypes.c_int
         lib.oracle_select_rank.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 4 + \
             [ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]
@@ -105,7 +108,7 @@ def split_sizes(N: int, M: int):
 class _Bound:
     """Keeps the numpy arrays alive while C holds pointers into them."""
 
-    def __init__(self, pb, cands):
+    def __init__(self, pb, cands, orders=None):
         from gen.problem import problem_arrays
         a = problem_arrays(pb)
         self.keep = dict(a)
@@ -117,8 +120,12 @@ class _Bound:
             "L", "K", "max_split", "w_max", "producer_mask", "tab_off", "tab_f", "tab_b", "tab_act", "tab_p2p",
             "chunk_off", "chunk_layers", "inst_off", "inst_units", "budget_kib")])
         self.c = cands
+        self.ord = None if orders is None else np.ascontiguousarray(orders, np.uint16)
+        if self.ord is not None:
+            assert self.ord.shape == (cands.count, pb.P, 2 * pb.n_max), self.ord.shape
         self.cs = _OCands(pb.n_max, pb.fbw, *[np.ascontiguousarray(getattr(cands, n)).ctypes.data
-                                              for n in ("split", "n", "fwd", "bwd", "fb")])
+                                              for n in ("split", "n", "fwd", "bwd", "fb")],
+                          None if self.ord is None else self.ord.ctypes.data)
 
 
 class Results:
@@ -131,14 +138,16 @@ class Results:
         self.busy = np.zeros(count, np.uint64)
 
 
-def evaluate(pb, cands, first: int = 0, count: Optional[int] = None, threads: int = 1) -> Results:
-    """O1-O10 for candidates [first, first+count) of the host-view batch `cands`."""
+def evaluate(pb, cands, first: int = 0, count: Optional[int] = None, threads: int = 1, orders=None) -> Results:
+    """O1-O10 for candidates [first, first+count) of the host-view batch `cands`; with `orders`
+    ([count_total, P, 2 n_max] u16, segment id | 0x8000 for backward, 0xFFFF beyond 2n: explicit
+    per-rank orders, f1's output) those replace the shared sequences + F/B bits (O4/O5)."""
     for n in ("split", "n", "fwd", "bwd", "fb"):
         assert getattr(cands, n).flags["C_CONTIGUOUS"], n
     if count is None:
         count = cands.count - first
     lib = _load()
-    bd = _Bound(pb, cands)
+    bd = _Bound(pb, cands, orders)
     res = Results(count, pb.P)
     lib.oracle_eval(ctypes.byref(bd.pb), ctypes.byref(bd.cs), first, count, res.makespan.ctypes.data,
                     res.status.ctypes.data, res.oom_mask.ctypes.data, res.bubble.ctypes.data,
@@ -148,8 +157,9 @@ def evaluate(pb, cands, first: int = 0, count: Optional[int] = None, threads: in
 
 def interleave(pb, cands, first: int = 0, count: Optional[int] = None, threads: int = 1):
     """I1-I6: DIP's dual-queue greedy interleaving of each candidate's split and
-    forward / backward priority orders (its F/B bits are ignored). Returns (bits, Results):
-    bits [count, P, fbw] in the host-view layout, and the score of the built schedule."""
+    forward / backward priority orders (its F/B bits are ignored). Returns (orders, Results):
+    orders [count, P, 2 n_max] u16 -- each rank's stage order, segment id | 0x8000 for a backward
+    stage, 0xFFFF beyond 2n -- and the score of the built schedule."""
     for nme in ("split", "n", "fwd", "bwd", "fb"):
         assert getattr(cands, nme).flags["C_CONTIGUOUS"], nme
     if count is None:
@@ -157,12 +167,28 @@ def interleave(pb, cands, first: int = 0, count: Optional[int] = None, threads: 
     lib = _load()
     bd = _Bound(pb, cands)
     res = Results(count, pb.P)
-    bits = np.zeros((count, pb.P, pb.fbw), np.uint32)
-    rc = lib.oracle_interleave(ctypes.byref(bd.pb), ctypes.byref(bd.cs), first, count, bits.ctypes.data,
+    ords = np.zeros((count, pb.P, 2 * pb.n_max), np.uint16)
+    rc = lib.oracle_interleave(ctypes.byref(bd.pb), ctypes.byref(bd.cs), first, count, ords.ctypes.data,
                                res.makespan.ctypes.data, res.status.ctypes.data, res.oom_mask.ctypes.data,
                                res.bubble.ctypes.data, res.peaks.ctypes.data, res.busy.ctypes.data, threads)
     assert rc == 0
-    return bits, res
+    return ords, res
+
+
+def mcts_table(Cn: int, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float, beta: float, table):
+    """S4-S6 alone with rollouts scored by table[seq[0], seq[1]] (a test fixture):
+    returns dict(trace [rounds], leaves [rounds, leaves] node ids, tree: parent, cls, N, s per node)."""
+    t = np.ascontiguousarray(np.asarray(table, np.float64).reshape(-1))
+    assert t.size == Cn * Cn
+    cap = 1 + rounds * leaves
+    trace = np.zeros(rounds, np.float64)
+    lv = np.zeros((rounds, leaves), np.int32)
+    par, cls, N, sv = np.zeros(cap, np.int32), np.zeros(cap, np.int32), np.zeros(cap, np.uint32), np.zeros(cap, np.float64)
+    lib = _load()
+    nn = lib.oracle_mcts_table(Cn, seed & ((1 << 64) - 1), rounds, leaves, rollouts, alpha, beta, t.ctypes.data,
+                               trace.ctypes.data, lv.ctypes.data, par.ctypes.data, cls.ctypes.data, N.ctypes.data,
+                               sv.ctypes.data)
+    return dict(trace=trace, leaves=lv, parent=par[:nn], cls=cls[:nn], N=N[:nn], s=sv[:nn])
 
 
 def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float = 1.0, beta: float = 0.5,
@@ -181,18 +207,19 @@ def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha:
     scored = ctypes.c_uint64()
     fwd = np.zeros(pb.n_max, np.uint16)
     bwd = np.zeros(pb.n_max, np.uint16)
-    bits = np.zeros((pb.P, pb.fbw), np.uint32)
+    ords = np.zeros((pb.P, 2 * pb.n_max), np.uint16)
     arrs = _menu_arrays(menu)                     # kept alive for the call
     lib.oracle_search(ctypes.byref(bd.pb), pb.n_max, pb.fbw, sp.ctypes.data, seed & ((1 << 64) - 1), rounds, leaves,
                       rollouts, alpha, beta, trace.ctypes.data, ctypes.byref(sc), ctypes.byref(mk), fwd.ctypes.data,
-                      bwd.ctypes.data, bits.ctypes.data, ctypes.byref(scored), *_menu_args(arrs, S))
-    return dict(score=sc.value, makespan=mk.value, trace=trace, fwd=fwd, bwd=bwd, bits=bits, scored=scored.value)
+                      bwd.ctypes.data, ords.ctypes.data, ctypes.byref(scored), *_menu_args(arrs, S))
+    return dict(score=sc.value, makespan=mk.value, trace=trace, fwd=fwd, bwd=bwd, orders=ords, scored=scored.value)
 
 
-def timeline(pb, cands, x: int):
-    """Per-(rank, slot) (start, end) arrays of candidate x, shape [P, 2n]; None unless timed."""
+def timeline(pb, cands, x: int, orders=None):
+    """Per-(rank, slot) (start, end) arrays of candidate x, shape [P, 2n]; None unless timed
+    (`orders`: explicit per-rank orders, as evaluate)."""
     lib = _load()
-    bd = _Bound(pb, cands)
+    bd = _Bound(pb, cands, orders)
     n = int(cands.n[x])
     st = np.zeros(max(1, pb.P * 2 * n), np.uint64)
     en = np.zeros_like(st)
@@ -251,18 +278,19 @@ def select_rank(sF, sB, cands, budget: int, gap_pm: int = 50, node_cap: int = 40
 
 
 def memopt(pb, cands, menu, S: int = 10, first: int = 0, count: Optional[int] = None, threads: int = 1,
-           gap_pm: int = 50, node_cap: int = 4096, stats: bool = False):
+           gap_pm: int = 50, node_cap: int = 4096, stats: bool = False, orders=None):
     """M1-M4: per-layer memory optimisation of each candidate schedule. `menu` =
     (f, b, act) arrays [n_strat, T] aligned with the model's tables. Returns (sel, Results) with
     sel [count, P, 2, n_max] the selected candidate index of each pair at forward position p
     (sel[..., 0, p]) and backward position q (sel[..., 1, q]) and the re-timed results. M3 solves
     each rank's ILP to a relative gap <= gap_pm per mille, at most node_cap B&B children.
-    With stats=True also returns [count, P, 5] per-rank (warm, bound, final, nodes, flags)."""
+    With stats=True also returns [count, P, 5] per-rank (warm, bound, final, nodes, flags). With
+    `orders` (explicit per-rank orders, as evaluate) the pairs come from those orders."""
     if count is None:
         count = cands.count - first
     f, b, a = (np.ascontiguousarray(v, np.uint32) for v in menu)
     lib = _load()
-    bd = _Bound(pb, cands)
+    bd = _Bound(pb, cands, orders)
     res = Results(count, pb.P)
     sel = np.zeros((count, pb.P, 2, pb.n_max), np.uint8)
     rst = np.zeros((count, pb.P, 5), np.uint64) if stats else None

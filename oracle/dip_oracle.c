@@ -51,6 +51,9 @@ typedef struct {
     const uint32_t *n;              /* [N] */
     const uint16_t *fwd, *bwd;      /* [N][n_max] */
     const uint32_t *fb;             /* [N][P][fbw] */
+    const uint16_t *ord;            /* NULL, or [N][P][2 n_max] explicit per-rank orders (segment id |
+                                       0x8000 for a backward stage; 0xFFFF beyond 2n) replacing the
+                                       shared sequences + F/B bits in O4/O5 (f1's output, R-29) */
 } ocands;
 
 enum { ST_OK = 0, ST_OOM = 1, ST_DEADLOCK = 2, ST_BAD = 3 };
@@ -158,7 +161,21 @@ static void eval_one(const oproblem *pb, const ocands *cs, uint64_t x, ores *res
         }
     /* O4: encoding checks */
     if (!bad && (ncand != n || n > n_max)) bad = 1;
-    if (!bad) {
+    const uint16_t *ord = cs->ord ? cs->ord + x * (uint64_t)P * 2 * n_max : NULL;
+    if (!bad && ord) {          /* explicit per-rank orders: every stage of the rank exactly once */
+        uint8_t *seen = malloc(2 * (size_t)(idmax + 1));
+        for (uint32_t r = 0; r < P && !bad; r++) {
+            memset(seen, 0, 2 * (size_t)(idmax + 1));
+            for (uint32_t t = 0; t < 2 * n_max && !bad; t++) {
+                uint32_t e = ord[(size_t)r * 2 * n_max + t], sg = e & 0x7FFFu, dr = e >> 15;
+                if (t >= 2 * n) { if (e != 0xFFFF) bad = 1; continue; }
+                if (sg >= idmax || !present[sg] || seen[dr * (idmax + 1) + sg]) bad = 1;
+                else seen[dr * (idmax + 1) + sg] = 1;
+            }
+        }
+        free(seen);
+    }
+    if (!bad && !ord) {
         uint8_t *seenF = calloc(idmax + 1, 1), *seenB = calloc(idmax + 1, 1);
         for (uint32_t p = 0; p < n_max && !bad; p++) {
             if (p < n) {
@@ -195,9 +212,17 @@ static void eval_one(const oproblem *pb, const ocands *cs, uint64_t x, ores *res
         for (uint32_t r = 0; r < P; r++) {
             uint32_t fi = 0, bi = 0;
             for (uint32_t t = 0; t < S; t++) {
-                uint32_t node = r * S + t, isb = (fb[r * fbw + t / 32] >> (t % 32)) & 1u, s;
-                if (isb) { s = bwd[bi++]; slotB[r * (idmax + 1) + s] = t; }
-                else { s = fwd[fi++]; slotF[r * (idmax + 1) + s] = t; }
+                uint32_t node = r * S + t, isb, s;
+                if (ord) {
+                    uint32_t e = ord[(size_t)r * 2 * n_max + t];
+                    isb = e >> 15;
+                    s = e & 0x7FFFu;
+                } else {
+                    isb = (fb[r * fbw + t / 32] >> (t % 32)) & 1u;
+                    s = isb ? bwd[bi++] : fwd[fi++];
+                }
+                if (isb) slotB[r * (idmax + 1) + s] = t;
+                else slotF[r * (idmax + 1) + s] = t;
                 dir[node] = (uint8_t)isb;
                 seg[node] = s;
                 uint32_t i = si[s], k = sk[s];
@@ -371,28 +396,40 @@ int oracle_timeline(const oproblem *pb, const ocands *cs, uint64_t x, uint64_t *
 /* ======================================================================================
  * I1-I6: DIP's greedy dual-queue stage interleaving (§5.2), the row f1 of
  * given a split and segment priorities (the forward and backward priority orders
- * = fwd_seq / bwd_seq of a candidate; its F/B bits are ignored), build every rank's F/B
- * interleaving and its timing. Readings: in-order queues (each rank's Q_fw / Q_bw
- * head is its next segment in priority order, R-26/A.8); a head's t_start is finite once all its
- * predecessors are placed; rank = argmin t_min, ties to the lowest rank;
- * step 3 "both t_fw < t_last and t_bw < t_last" strict, alternating on the last type;
- * step 4 smallest t_start, ties to the backward (R-29); memory gating: the forward
- * queue is disabled while placing its head would exceed the rank's budget (R-30); if every rank
- * is blocked only by gating, the gate is lifted for one step (R-31), the overflow shows as OOM.
+ * = fwd_seq / bwd_seq of a candidate: position p = priority rank, 0 highest; its F/B bits are
+ * ignored), build every rank's stage order and its timing. Readings:
+ *   I1 the split and the priority orders are validated as O2-O4 (else BAD_ENCODING).
+ *   I2 stage costs as O6.
+ *   I3 every rank keeps two priority queues of its unscheduled forward / backward stages
+ *      (P:527-528); a stage's t_start is finite once all its predecessors (the cross-rank edges of
+ *      O7) are scheduled: the max over them of end + transfer; the queue's minimum
+ *      start time t_fw / t_bw is the min over its stages ("among stages in Q_fw and Q_bw",
+ *      reading R-29: every queued stage counts, the queue's priority orders its ready stages).
+ *   I4 memory gating (R-30): a forward stage whose activation would take the rank
+ *      above its budget is disabled (not counted in t_fw and not schedulable).
+ *   I5 the rank with the smallest t_min = min(t_fw, t_bw), ties to the lowest rank; if
+ *      every rank is blocked by its gates only, the gates are lifted for one step (R-31: the rank
+ *      of the smallest gated forward t_start) and the overflow shows as OOM.
+ *   I6 steps 2-4: the direction -- if t_fw < t_last and t_bw < t_last, alternate on
+ *      the last scheduled type (1F1B emulation; forward first), otherwise the queue of the smaller
+ *      minimum start time (step 4 "the stage with the smallest t_start", ties to the backward,
+ *      R-29) -- then that queue's highest-priority stage among those that start as early as its
+ *      earliest one (t_start <= max(t_dir, t_last)). The stage starts at max(t_start, t_last).
+ * The stage DAG is acyclic, so every step schedules a stage: no DEADLOCK. The output is each
+ * rank's order: ord[r][t] = segment id | direction << 15 (1 = backward).
  * ====================================================================================== */
-typedef struct { uint64_t end; uint8_t placed; } inode;
-
-static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uint32_t *bits_out /* [P][fbw] */,
+#define ORD_B 0x8000u
+static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uint16_t *ord_out /* [P][2 n_max] */,
                            ores *res, uint64_t *peaks) {
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
-    const uint32_t n_max = cs->n_max, fbw = cs->fbw;
+    const uint32_t n_max = cs->n_max;
     const uint8_t *split = cs->split + x * (uint64_t)m * nm;
     const uint16_t *fwd = cs->fwd + x * (uint64_t)n_max;
     const uint16_t *bwd = cs->bwd + x * (uint64_t)n_max;
     const uint32_t ncand = cs->n[x];
     res->makespan = UINT64_MAX; res->busy = 0; res->status = ST_BAD; res->oom_mask = 0; res->bubble = -1.0;
     for (uint32_t r = 0; r < P; r++) { if (peaks) peaks[r] = 0; }
-    memset(bits_out, 0, sizeof(uint32_t) * P * fbw);
+    for (size_t t = 0; t < (size_t)P * 2 * n_max; t++) ord_out[t] = 0xFFFF;
 
     /* I1 (= O1-O4 without the bit strings): segment ids, split, work units, sequences */
     uint32_t idmax = seg_count_max(pb);
@@ -401,6 +438,7 @@ static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uin
     uint8_t *present = calloc(idmax + 1, 1);
     uint32_t *sb = malloc(sizeof(uint32_t) * (idmax + 1)), *si = malloc(sizeof(uint32_t) * (idmax + 1));
     uint32_t *sj = malloc(sizeof(uint32_t) * (idmax + 1)), *sk = malloc(sizeof(uint32_t) * (idmax + 1));
+    uint32_t *prio = malloc(sizeof(uint32_t) * 2 * (idmax + 1));     /* [dir][s]: position in its order */
     int bad = 0;
     uint32_t acc = 0, n = 0;
     for (uint32_t b = 0; b < m; b++)
@@ -438,7 +476,7 @@ static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uin
             if (p < n) {
                 uint32_t a = fwd[p], c = bwd[p];
                 if (a >= idmax || c >= idmax || !present[a] || !present[c] || seenF[a] || seenB[c]) bad = 1;
-                else { seenF[a] = 1; seenB[c] = 1; }
+                else { seenF[a] = 1; seenB[c] = 1; prio[a] = p; prio[idmax + 1 + c] = p; }
             } else if (fwd[p] != 0xFFFF || bwd[p] != 0xFFFF) bad = 1;
         }
         free(seenF); free(seenB);
@@ -446,112 +484,139 @@ static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uin
     if (bad) goto done;
     if (n == 0) { res->makespan = 0; res->status = ST_OK; res->bubble = 0.0; goto done; }
     {
-        /* node (dir, s, r) -> index (r * 2 + dir) * idmax + s */
-        const uint32_t NN = P * 2 * idmax;
-        inode *nd = calloc(NN, sizeof(inode));
-#define NODE(dir, s, r) (((r) * 2u + (dir)) * idmax + (s))
-        uint32_t *fi = calloc(P, sizeof(uint32_t)), *bi = calloc(P, sizeof(uint32_t));
-        uint64_t *tlast = calloc(P, sizeof(uint64_t)), *cur = calloc(P, sizeof(uint64_t)), *pk = calloc(P, sizeof(uint64_t));
-        int *last = malloc(sizeof(int) * P);
-        for (uint32_t r = 0; r < P; r++) last[r] = -1;
-        uint64_t mk = 0, busy = 0;
-        int dead = 0;
-        /* I2: stage costs (as O6) */
+        /* node (dir, s, r) -> index (r * 2 + dir) * (idmax + 1) + s */
+        const uint32_t IS = idmax + 1, NN = P * 2 * IS;
+#define NODE(dir, s, r) (((r) * 2u + (dir)) * IS + (s))
 #define LAYERS(i, k, r) ((uint64_t)layers_of(pb, (i), (k) * P + (r)))
 #define LAT(dir, s, r) (LAYERS(si[s], sk[s], r) * (uint64_t)((dir) ? pb->tab_b[pb->tab_off[si[s]] + W[s]] : pb->tab_f[pb->tab_off[si[s]] + W[s]]))
 #define ACT(s, r) (LAYERS(si[s], sk[s], r) * (uint64_t)pb->tab_act[pb->tab_off[si[s]] + W[s]])
 #define P2P(s) ((uint64_t)pb->tab_p2p[pb->tab_off[si[s]] + W[s]])
-        for (uint32_t step = 0; step < P * 2 * n; step++) {
-            /* I3: per rank, the t_start of both queue heads (UINT64_MAX = not ready / empty) */
-            uint64_t tf[32], tb[32];
-            int gated[32];
+        uint32_t *indeg = calloc(NN, sizeof(uint32_t));   /* predecessors not yet scheduled */
+        uint64_t *tst = calloc(NN, sizeof(uint64_t));     /* running max of pred end + transfer */
+        uint64_t *endt = calloc(NN, sizeof(uint64_t));
+        /* per rank and direction: the ready list (segment ids) */
+        uint32_t *rl = malloc(sizeof(uint32_t) * (size_t)P * 2 * IS), *rc = calloc(P * 2, sizeof(uint32_t));
+        uint64_t *tlast = calloc(P, sizeof(uint64_t)), *cur = calloc(P, sizeof(uint64_t)), *pk = calloc(P, sizeof(uint64_t));
+        uint32_t *cnt = calloc(P, sizeof(uint32_t));
+        int *last = malloc(sizeof(int) * P);
+        for (uint32_t r = 0; r < P; r++) last[r] = -1;
+        /* I3: predecessor counts (the cross-rank edges of O7; succ() below enumerates the same edges) */
+        for (uint32_t s = 0; s < idmax; s++) {
+            if (!present[s]) continue;
+            uint32_t b = sb[s], i = si[s], k = sk[s], K = pb->K[i];
             for (uint32_t r = 0; r < P; r++) {
-                for (int dir = 0; dir < 2; dir++) {
-                    uint32_t h = dir ? bi[r] : fi[r];
-                    uint64_t ts = UINT64_MAX;
-                    if (h < n) {
-                        uint32_t s = dir ? bwd[h] : fwd[h];
-                        uint32_t b = sb[s], i = si[s], k = sk[s], K = pb->K[i];
-                        int ok = 1;
-                        uint64_t t0 = 0;
-                        /* cross-rank predecessors, exactly the edges of O7 (the rank order is what
-                         * this algorithm decides, so there is no same-rank chain edge here) */
-#define DEP(nid, wgt) do { inode *pn = &nd[nid]; if (!pn->placed) ok = 0; else if (pn->end + (wgt) > t0) t0 = pn->end + (wgt); } while (0)
-                        if (dir == 0) {
-                            if (r > 0) DEP(NODE(0, s, r - 1), P2P(s));
-                            else if (k > 0) DEP(NODE(0, s - 1, P - 1), P > 1 ? P2P(s - 1) : 0);
-                            else for (uint32_t ip = 0; ip < nm; ip++) {
-                                if (!((pb->producer_mask[i] >> ip) & 1u)) continue;
-                                for (uint32_t jp = 0; jp < split[b * nm + ip]; jp++) {
-                                    uint32_t pr = base[b * nm + ip] + jp * pb->K[ip] + pb->K[ip] - 1;
-                                    DEP(NODE(0, pr, P - 1), P > 1 ? P2P(pr) : 0);
-                                }
-                            }
-                        } else {
-                            if (r + 1 < P) DEP(NODE(1, s, r + 1), P2P(s));
-                            else if (k + 1 < K) DEP(NODE(1, s + 1, 0), P > 1 ? P2P(s) : 0);
-                            else {
-                                int any = 0;
-                                for (uint32_t ic = 0; ic < nm; ic++) {
-                                    if (!((pb->producer_mask[ic] >> i) & 1u)) continue;
-                                    for (uint32_t jc = 0; jc < split[b * nm + ic]; jc++) {
-                                        DEP(NODE(1, base[b * nm + ic] + jc * pb->K[ic], 0), P > 1 ? P2P(s) : 0);
-                                        any = 1;
-                                    }
-                                }
-                                if (!any) DEP(NODE(0, s, P - 1), 0);
-                            }
-                        }
-#undef DEP
-                        if (ok) ts = t0;
-                    }
-                    if (dir) tb[r] = ts; else tf[r] = ts;
+                uint32_t dF = 0, dB = 0;
+                if (r > 0) dF = 1;
+                else if (k > 0) dF = 1;
+                else for (uint32_t ip = 0; ip < nm; ip++) if ((pb->producer_mask[i] >> ip) & 1u) dF += split[b * nm + ip];
+                if (r + 1 < P) dB = 1;
+                else if (k + 1 < K) dB = 1;
+                else {
+                    for (uint32_t ic = 0; ic < nm; ic++) if ((pb->producer_mask[ic] >> i) & 1u) dB += split[b * nm + ic];
+                    if (dB == 0) dB = 1;                                 /* loss turnaround (R-6) */
                 }
-                /* I4: memory gating: the forward queue is disabled while placing its
-                 * head would exceed the rank's budget (R-30) */
-                gated[r] = 0;
-                if (tf[r] != UINT64_MAX && cur[r] + ACT(fwd[fi[r]], r) > pb->budget_kib[r]) gated[r] = 1;
+                indeg[NODE(0, s, r)] = dF;
+                indeg[NODE(1, s, r)] = dB;
+                if (dF == 0) rl[(r * 2 + 0) * IS + rc[r * 2 + 0]++] = s;
             }
-            /* I5: the rank with the smallest t_min, ties to the lowest rank */
+        }
+        uint64_t mk = 0, busy = 0;
+        int dead = 0;
+        for (uint32_t step = 0; step < P * 2 * n; step++) {
+            /* I3 / I4: per rank, t_fw over its ungated ready forwards, t_bw over its ready backwards,
+               and the smallest forward t_start regardless of the gate (for R-31) */
+            uint64_t tf[32], tb[32], tg[32];
+            for (uint32_t r = 0; r < P; r++) {
+                tf[r] = tb[r] = tg[r] = UINT64_MAX;
+                for (uint32_t a = 0; a < rc[r * 2 + 0]; a++) {
+                    uint32_t s = rl[(r * 2 + 0) * IS + a];
+                    uint64_t t = tst[NODE(0, s, r)];
+                    if (t < tg[r]) tg[r] = t;
+                    if (cur[r] + ACT(s, r) <= pb->budget_kib[r] && t < tf[r]) tf[r] = t;
+                }
+                for (uint32_t a = 0; a < rc[r * 2 + 1]; a++) {
+                    uint64_t t = tst[NODE(1, rl[(r * 2 + 1) * IS + a], r)];
+                    if (t < tb[r]) tb[r] = t;
+                }
+            }
+            /* I5 */
             int rr = -1, relax = 0;
             uint64_t best = UINT64_MAX;
             for (uint32_t r = 0; r < P; r++) {
-                uint64_t f = gated[r] ? UINT64_MAX : tf[r];
-                uint64_t tm = f < tb[r] ? f : tb[r];
+                uint64_t tm = tf[r] < tb[r] ? tf[r] : tb[r];
                 if (tm < best) { best = tm; rr = (int)r; }
             }
-            if (rr < 0) {   /* every rank blocked by the gate only: lift it for one step (R-31) */
-                for (uint32_t r = 0; r < P; r++) {
-                    uint64_t tm = tf[r] < tb[r] ? tf[r] : tb[r];
-                    if (tm < best) { best = tm; rr = (int)r; }
-                }
+            if (rr < 0) {                       /* every rank blocked by its gates only (R-31) */
+                for (uint32_t r = 0; r < P; r++)
+                    if (tg[r] < best) { best = tg[r]; rr = (int)r; }
                 relax = 1;
             }
-            if (rr < 0) { dead = 1; break; }
+            if (rr < 0) { dead = 1; break; }    /* unreachable: the stage DAG is acyclic */
             const uint32_t r = (uint32_t)rr;
-            const uint64_t f = (gated[r] && !relax) ? UINT64_MAX : tf[r], bb = tb[r];
-            /* I6: steps 2-4 */
+            const uint64_t fmin = relax ? tg[r] : tf[r], bmin = tb[r];
+            /* I6: the direction (step 3: alternate; step 4: the smaller of t_fw / t_bw, ties to the
+               backward), then that queue's highest-priority stage among those that start as early as
+               its earliest one, i.e. with t_start <= max(t_dir, t_last) */
             int dir;
-            if (f != UINT64_MAX && bb != UINT64_MAX && f < tlast[r] && bb < tlast[r])
-                dir = last[r] == 0 ? 1 : 0;                 /* emulate 1F1B: alternate */
-            else if (f == UINT64_MAX) dir = 1;
-            else if (bb == UINT64_MAX) dir = 0;
-            else dir = bb <= f ? 1 : 0;                     /* smallest t_start; ties -> backward (R-29) */
-            uint32_t h = dir ? bi[r] : fi[r];
-            uint32_t s = dir ? bwd[h] : fwd[h];
-            uint64_t ts = dir ? bb : f;
-            uint64_t st = ts > tlast[r] ? ts : tlast[r];
-            uint64_t lat = LAT(dir, s, r);
-            uint64_t en = st + lat;
-            nd[NODE(dir, s, r)].end = en;
-            nd[NODE(dir, s, r)].placed = 1;
+            if (fmin != UINT64_MAX && bmin != UINT64_MAX && fmin < tlast[r] && bmin < tlast[r])
+                dir = last[r] == 0 ? 1 : 0;                         /* emulate 1F1B: alternate */
+            else if (fmin == UINT64_MAX) dir = 1;
+            else if (bmin == UINT64_MAX) dir = 0;
+            else dir = bmin <= fmin ? 1 : 0;                        /* smallest t_start; ties -> B */
+            const uint64_t tdir = dir ? bmin : fmin, lim = tdir > tlast[r] ? tdir : tlast[r];
+            uint32_t pick = 0, bp = UINT32_MAX;
+            for (uint32_t a = 0; a < rc[r * 2 + dir]; a++) {
+                uint32_t s = rl[(r * 2 + dir) * IS + a];
+                if (tst[NODE(dir, s, r)] > lim) continue;
+                if (dir == 0 && !relax && cur[r] + ACT(s, r) > pb->budget_kib[r]) continue;
+                if (prio[dir * IS + s] < bp) { bp = prio[dir * IS + s]; pick = s; }
+            }
+            /* place (dir, pick) on rank r */
+            const uint32_t s = pick, nd = NODE(dir, s, r);
+            for (uint32_t a = 0; a < rc[r * 2 + dir]; a++)          /* dequeue */
+                if (rl[(r * 2 + dir) * IS + a] == s) { rl[(r * 2 + dir) * IS + a] = rl[(r * 2 + dir) * IS + --rc[r * 2 + dir]]; break; }
+            uint64_t st = tst[nd] > tlast[r] ? tst[nd] : tlast[r];
+            uint64_t lat = LAT(dir, s, r), en = st + lat;
+            endt[nd] = en;
             tlast[r] = en;
             last[r] = dir;
             busy += lat;
             if (en > mk) mk = en;
-            uint32_t t = fi[r] + bi[r];
-            if (dir) { bits_out[r * fbw + t / 32] |= 1u << (t % 32); bi[r]++; cur[r] -= ACT(s, r); }
-            else { fi[r]++; cur[r] += ACT(s, r); if (cur[r] > pk[r]) pk[r] = cur[r]; }
+            ord_out[(size_t)r * 2 * n_max + cnt[r]++] = (uint16_t)(s | (dir ? ORD_B : 0u));
+            if (dir) cur[r] -= ACT(s, r);
+            else { cur[r] += ACT(s, r); if (cur[r] > pk[r]) pk[r] = cur[r]; }
+            /* successors (the edges of O7): their t_start and readiness */
+            uint32_t b = sb[s], i = si[s], k = sk[s], K = pb->K[i];
+#define RELEASE(D2, S2, R2, WT) do { uint32_t v_ = NODE((D2), (S2), (R2)); \
+            if (en + (WT) > tst[v_]) tst[v_] = en + (WT); \
+            if (--indeg[v_] == 0) rl[((R2) * 2 + (D2)) * IS + rc[(R2) * 2 + (D2)]++] = (S2); } while (0)
+            if (dir == 0) {
+                if (r + 1 < P) RELEASE(0, s, r + 1, P2P(s));
+                else if (k + 1 < K) RELEASE(0, s + 1, 0, P > 1 ? P2P(s) : 0);
+                else {
+                    int any = 0;
+                    for (uint32_t ic = 0; ic < nm; ic++) {
+                        if (!((pb->producer_mask[ic] >> i) & 1u)) continue;
+                        for (uint32_t jc = 0; jc < split[b * nm + ic]; jc++) {
+                            RELEASE(0, base[b * nm + ic] + jc * pb->K[ic], 0, P > 1 ? P2P(s) : 0);
+                            any = 1;
+                        }
+                    }
+                    if (!any) RELEASE(1, s, P - 1, 0);                   /* loss turnaround (R-6) */
+                }
+            } else {
+                if (r > 0) RELEASE(1, s, r - 1, P2P(s));
+                else if (k > 0) RELEASE(1, s - 1, P - 1, P > 1 ? P2P(s - 1) : 0);
+                else
+                    for (uint32_t ip = 0; ip < nm; ip++) {
+                        if (!((pb->producer_mask[i] >> ip) & 1u)) continue;
+                        for (uint32_t jp = 0; jp < split[b * nm + ip]; jp++) {
+                            uint32_t pr = base[b * nm + ip] + jp * pb->K[ip] + pb->K[ip] - 1;
+                            RELEASE(1, pr, P - 1, P > 1 ? P2P(pr) : 0);
+                        }
+                    }
+            }
+#undef RELEASE
         }
         uint32_t oom = 0;
         for (uint32_t r = 0; r < P; r++) {
@@ -573,17 +638,17 @@ static void interleave_one(const oproblem *pb, const ocands *cs, uint64_t x, uin
 #undef ACT
 #undef P2P
 #undef NODE
-        free(nd); free(fi); free(bi); free(tlast); free(cur); free(pk); free(last);
+        free(indeg); free(tst); free(endt); free(rl); free(rc); free(tlast); free(cur); free(pk); free(cnt); free(last);
     }
 done:
-    free(base); free(W); free(present); free(sb); free(si); free(sj); free(sk);
+    free(base); free(W); free(present); free(sb); free(si); free(sj); free(sk); free(prio);
 }
 
 typedef struct {
     const oproblem *pb;
     const ocands *cs;
     uint64_t lo, hi, first;
-    uint32_t *bits;
+    uint16_t *ord;
     uint64_t *makespan, *busy, *peaks;
     uint32_t *status, *oom;
     double *bubble;
@@ -591,20 +656,20 @@ typedef struct {
 
 static void *iworker(void *arg) {
     ijob_t *j = (ijob_t *)arg;
-    const uint32_t P = j->pb->P, fbw = j->cs->fbw;
+    const uint32_t P = j->pb->P, n_max = j->cs->n_max;
     for (uint64_t x = j->lo; x < j->hi; x++) {
         ores r;
         uint64_t o = x - j->first;
-        interleave_one(j->pb, j->cs, x, j->bits + o * P * fbw, &r, j->peaks ? j->peaks + o * P : NULL);
+        interleave_one(j->pb, j->cs, x, j->ord + o * P * 2 * n_max, &r, j->peaks ? j->peaks + o * P : NULL);
         j->makespan[o] = r.makespan; j->busy[o] = r.busy; j->status[o] = r.status;
         j->oom[o] = r.oom_mask; j->bubble[o] = r.bubble;
     }
     return NULL;
 }
 
-/* Interleave candidates [first, first+count): writes each one's F/B bits ([count][P][fbw]) and
- * the resulting schedule's score (as oracle_eval). */
-int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint64_t count, uint32_t *bits,
+/* Interleave candidates [first, first+count): writes each one's per-rank orders
+ * ([count][P][2 n_max], id | 0x8000 for backward) and the resulting schedule's score (as oracle_eval). */
+int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint64_t count, uint16_t *ord,
                       uint64_t *makespan, uint32_t *status, uint32_t *oom_mask, double *bubble, uint64_t *peaks,
                       uint64_t *busy, int threads) {
     if (pb->P > 32) return -1;
@@ -618,7 +683,7 @@ int oracle_interleave(const oproblem *pb, const ocands *cs, uint64_t first, uint
         uint64_t lo = first + per * t, hi = lo + per;
         if (hi > first + count) hi = first + count;
         if (lo > hi) lo = hi;
-        jobs[t] = (ijob_t){pb, cs, lo, hi, first, bits, makespan, busy, peaks, status, oom_mask, bubble};
+        jobs[t] = (ijob_t){pb, cs, lo, hi, first, ord, makespan, busy, peaks, status, oom_mask, bubble};
         pthread_create(&th[t], NULL, iworker, &jobs[t]);
     }
     for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
@@ -731,10 +796,190 @@ static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *ba
     free(indeg); free(key); free(ready);
 }
 
+/* S4-S6 + the rollout draws: the MCTS loop over sequences of Cn classes, with the rollout scoring
+ * (S3) left to `score` (count sequences [count][Cn] -> scores). Returns the number of tree nodes;
+ * optional outputs: trace [rounds] best score after each round, leaves_out [rounds][leaves] the
+ * selected / expanded leaf of every slot, the tree (parent, class, N, s) of every node. */
+typedef void (*mcts_score_fn)(void *ctx, uint32_t count, const uint32_t *seqs, const int *owner, double *scores);
+static uint32_t mcts_run(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t leaves, uint32_t rollouts,
+                         double alpha, double beta, mcts_score_fn score, void *ctx, double *trace,
+                         int32_t *leaves_out, int32_t *t_parent, int32_t *t_cls, uint32_t *t_N, double *t_s,
+                         uint64_t *scored_out) {
+    uint32_t ncap = 1 + rounds * leaves, nn = 1;
+    snode *T = calloc(ncap, sizeof(snode));
+    T[0].parent = -1; T[0].cls = -1; T[0].depth = 0;
+    uint32_t maxr = leaves * rollouts;
+    uint32_t *seqs = malloc(sizeof(uint32_t) * (size_t)(maxr ? maxr : 1) * Cn);
+    double *sc = malloc(sizeof(double) * (maxr ? maxr : 1));
+    int *owner = malloc(sizeof(int) * (maxr ? maxr : 1)), *leaf = malloc(sizeof(int) * leaves);
+    uint32_t *seq = malloc(sizeof(uint32_t) * Cn), *rest = malloc(sizeof(uint32_t) * Cn);
+    uint8_t *used = malloc(Cn);
+    double best = -1.0;
+    uint64_t u = 0;
+    *scored_out = 0;
+    for (uint32_t rd = 0; rd < rounds; rd++) {
+        uint32_t cnt = 0;
+        for (uint32_t l = 0; l < leaves; l++) {
+            int v = 0;
+            memset(used, 0, Cn);
+            for (;;) {                                           /* S4 / S5 */
+                snode *nd = &T[v];
+                if ((uint32_t)nd->depth == Cn) break;
+                if ((uint32_t)nd->nch < Cn - nd->depth) {        /* S5: the next unused class */
+                    uint32_t c, seen = 0;
+                    for (c = 0; c < Cn; c++) { if (used[c]) continue; if (seen++ == (uint32_t)nd->nch) break; }
+                    int id = (int)nn++;
+                    T[id].parent = v; T[id].cls = (int)c; T[id].depth = nd->depth + 1;
+                    if (nd->nch == nd->cap) { nd->cap = nd->cap ? 2 * nd->cap : 4; nd->ch = realloc(nd->ch, sizeof(int) * nd->cap); }
+                    nd->ch[nd->nch++] = id;
+                    used[c] = 1;
+                    v = id;
+                    break;
+                }
+                double Nx = (double)(nd->N + nd->vl), bu = -1.0;   /* S4: UCB */
+                int bc = -1;
+                for (int x = 0; x < nd->nch; x++) {
+                    snode *cn = &T[nd->ch[x]];
+                    double Nv = (double)(cn->N + cn->vl);
+                    double ucb = pow(cn->s, alpha) + beta * sqrt(log(Nx) / Nv);
+                    if (ucb > bu) { bu = ucb; bc = nd->ch[x]; }
+                }
+                used[T[bc].cls] = 1;
+                v = bc;
+            }
+            for (int x = v; x >= 0; x = T[x].parent) T[x].vl++;
+            leaf[l] = v;
+            if (leaves_out) leaves_out[rd * leaves + l] = v;
+            uint32_t d = (uint32_t)T[v].depth;
+            for (int x = v; x > 0; x = T[x].parent) seq[T[x].depth - 1] = (uint32_t)T[x].cls;
+            uint32_t trials = d == Cn ? 1 : rollouts;
+            for (uint32_t tr = 0; tr < trials; tr++) {           /* rollouts: random completions */
+                uint32_t nr = 0;
+                for (uint32_t c = 0; c < Cn; c++) {
+                    int on = 0;
+                    for (uint32_t p = 0; p < d; p++) if (seq[p] == c) on = 1;
+                    if (!on) rest[nr++] = c;
+                }
+                uint64_t rs = smix(seed ^ smix(u + 0x51A9u));
+                for (uint32_t x = nr; x > 1; x--) {
+                    rs += 0x9E3779B97F4A7C15ull;
+                    uint32_t y = (uint32_t)(smix(rs) % x), t2 = rest[x - 1];
+                    rest[x - 1] = rest[y]; rest[y] = t2;
+                }
+                for (uint32_t x = 0; x < nr; x++) seq[d + x] = rest[x];
+                memcpy(seqs + (size_t)cnt * Cn, seq, sizeof(uint32_t) * Cn);
+                owner[cnt] = (int)l;
+                cnt++;
+                u++;
+            }
+        }
+        score(ctx, cnt, seqs, owner, sc);                        /* S3 */
+        double *lb = calloc(leaves, sizeof(double));
+        for (uint32_t x = 0; x < cnt; x++) {
+            if (sc[x] > lb[owner[x]]) lb[owner[x]] = sc[x];
+            if (sc[x] > best) best = sc[x];
+        }
+        *scored_out += cnt;
+        for (uint32_t l = 0; l < leaves; l++)                       /* S6 */
+            for (int x = leaf[l]; x >= 0; x = T[x].parent) {
+                if (lb[l] > T[x].s) T[x].s = lb[l];
+                T[x].N++;
+                T[x].vl--;
+            }
+        free(lb);
+        if (trace) trace[rd] = best;
+    }
+    for (uint32_t x = 0; x < nn; x++) {
+        if (t_parent) t_parent[x] = T[x].parent;
+        if (t_cls) t_cls[x] = T[x].cls;
+        if (t_N) t_N[x] = T[x].N;
+        if (t_s) t_s[x] = T[x].s;
+        free(T[x].ch);
+    }
+    free(T); free(seqs); free(sc); free(owner); free(leaf); free(seq); free(rest); free(used);
+    return nn;
+}
+
+/* The MCTS loop alone, scored by a table over the first two classes of a sequence:
+ * score(seq) = table[seq[0] * Cn + seq[1]] (a test fixture for S4-S6, independent of f1). */
+typedef struct { uint32_t Cn; const double *table; } tab_ctx;
+static void tab_score(void *ctx, uint32_t count, const uint32_t *seqs, const int *owner, double *scores) {
+    (void)owner;
+    tab_ctx *t = (tab_ctx *)ctx;
+    for (uint32_t x = 0; x < count; x++) {
+        const uint32_t *q = seqs + (size_t)x * t->Cn;
+        scores[x] = t->table[q[0] * t->Cn + (t->Cn > 1 ? q[1] : 0)];
+    }
+}
+uint32_t oracle_mcts_table(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t leaves, uint32_t rollouts,
+                           double alpha, double beta, const double *table, double *trace, int32_t *leaves_out,
+                           int32_t *t_parent, int32_t *t_cls, uint32_t *t_N, double *t_s) {
+    tab_ctx c = {Cn, table};
+    uint64_t scored;
+    return mcts_run(Cn, seed, rounds, leaves, rollouts, alpha, beta, tab_score, &c, trace, leaves_out, t_parent,
+                    t_cls, t_N, t_s, &scored);
+}
+
+/* S1-S3 for oracle_search: a class sequence -> priority orders (S2) -> interleaving (I1-I6, orders)
+ * -> optionally M1-M4 -> LB / makespan */
+typedef struct {
+    const oproblem *pb;
+    const omenu *mn;
+    uint32_t n_max, fbw, n, C, Cn;
+    const uint8_t *split;
+    const uint32_t *base;
+    const int *clsof;
+    double LB, best;
+    uint64_t *best_makespan;
+    uint16_t *best_fwd, *best_bwd, *best_ord;
+} srch_ctx;
+
+static void search_score(void *ctxp, uint32_t cnt, const uint32_t *seqs, const int *owner, double *scores) {
+    (void)owner;
+    srch_ctx *c = (srch_ctx *)ctxp;
+    const oproblem *pb = c->pb;
+    const uint32_t P = pb->P, nm = pb->nmod, m = pb->m, n_max = c->n_max, Cn = c->Cn;
+    uint8_t *spl = malloc((size_t)(cnt ? cnt : 1) * m * nm);
+    uint32_t *nn_ = malloc(sizeof(uint32_t) * (cnt ? cnt : 1)), *prio = malloc(sizeof(uint32_t) * Cn);
+    uint16_t *fw = malloc(sizeof(uint16_t) * (size_t)(cnt ? cnt : 1) * n_max), *bw = malloc(sizeof(uint16_t) * (size_t)(cnt ? cnt : 1) * n_max);
+    uint32_t *fb = calloc((size_t)(cnt ? cnt : 1) * P * c->fbw, sizeof(uint32_t));
+    uint16_t *ord = malloc(sizeof(uint16_t) * (size_t)(cnt ? cnt : 1) * P * 2 * n_max);
+    for (uint32_t x = 0; x < cnt; x++) {
+        for (uint32_t p = 0; p < Cn; p++) prio[seqs[(size_t)x * Cn + p]] = Cn - 1 - p;   /* S2 */
+        memcpy(spl + (size_t)x * m * nm, c->split, m * nm);
+        nn_[x] = c->n;
+        s_order(pb, c->split, c->base, c->clsof, c->C, Cn, prio, 0, n_max, fw + (size_t)x * n_max);
+        s_order(pb, c->split, c->base, c->clsof, c->C, Cn, prio, 1, n_max, bw + (size_t)x * n_max);
+    }
+    ocands cs = {n_max, c->fbw, spl, nn_, fw, bw, fb, NULL};
+    for (uint32_t x = 0; x < cnt; x++) {
+        ores r;
+        uint16_t *ox = ord + (size_t)x * P * 2 * n_max;
+        interleave_one(pb, &cs, x, ox, &r, NULL);
+        if (c->mn->n_strat && r.status != ST_BAD) {           /* then per-layer memory opt. */
+            ocands c1 = {n_max, c->fbw, spl + (size_t)x * m * nm, nn_ + x, fw + (size_t)x * n_max,
+                         bw + (size_t)x * n_max, fb + (size_t)x * P * c->fbw, ox};
+            uint8_t *sel = malloc((size_t)P * 2 * n_max);
+            memopt_one(pb, c->mn, &c1, 0, sel, &r, NULL, NULL);
+            free(sel);
+        }
+        double sc = r.status == ST_OK ? c->LB / (double)r.makespan : 0.0;
+        scores[x] = sc;
+        if (sc > c->best) {
+            c->best = sc;
+            *c->best_makespan = r.makespan;
+            if (c->best_fwd) memcpy(c->best_fwd, fw + (size_t)x * n_max, sizeof(uint16_t) * n_max);
+            if (c->best_bwd) memcpy(c->best_bwd, bw + (size_t)x * n_max, sizeof(uint16_t) * n_max);
+            if (c->best_ord) memcpy(c->best_ord, ox, sizeof(uint16_t) * P * 2 * n_max);
+        }
+    }
+    free(spl); free(nn_); free(prio); free(fw); free(bw); free(fb); free(ord);
+}
+
 int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_t *split, uint64_t seed,
                   uint32_t rounds, uint32_t leaves, uint32_t rollouts, double alpha, double beta,
                   double *trace, double *best_score, uint64_t *best_makespan, uint16_t *best_fwd,
-                  uint16_t *best_bwd, uint32_t *best_bits, uint64_t *scored_out,
+                  uint16_t *best_bwd, uint16_t *best_ord /* [P][2 n_max] */, uint64_t *scored_out,
                   uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma, uint32_t S) {
     omenu mn = {n_strat, S, mf, mb, ma, 50, 4096};   /* n_strat = 0: rollouts are interleaved only */
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
@@ -744,7 +989,7 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
     for (uint32_t q = 0; q < m * nm; q++) {
         base[q] = acc;
         acc += pb->max_split[q % nm] * pb->K[q % nm];
-        clsof[q] = split[q] ? (int)C : -1;                   /* classes (b, i, 0..K_i-1) */
+        clsof[q] = split[q] ? (int)C : -1;                   /* S1: classes (b, i, 0..K_i-1) */
         if (split[q]) C += pb->K[q % nm];
         n += split[q] * pb->K[q % nm];
     }
@@ -772,116 +1017,12 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
         }
         if ((double)tot > LB) LB = (double)tot;
     }
-    uint32_t ncap = 1 + rounds * leaves, nn = 1;
-    snode *T = calloc(ncap, sizeof(snode));
-    T[0].parent = -1; T[0].cls = -1; T[0].depth = 0;
-    uint32_t maxr = leaves * rollouts;
-    uint8_t *spl = malloc((size_t)maxr * m * nm);
-    uint32_t *nn_ = malloc(sizeof(uint32_t) * maxr);
-    uint16_t *fw = malloc(sizeof(uint16_t) * (size_t)maxr * n_max), *bw = malloc(sizeof(uint16_t) * (size_t)maxr * n_max);
-    uint32_t *fb = calloc((size_t)maxr * P * fbw, sizeof(uint32_t)), *bits = malloc(sizeof(uint32_t) * (size_t)maxr * P * fbw);
-    int *owner = malloc(sizeof(int) * maxr), *leaf = malloc(sizeof(int) * leaves);
-    uint32_t *seq = malloc(sizeof(uint32_t) * Cn), *prio = malloc(sizeof(uint32_t) * Cn), *rest = malloc(sizeof(uint32_t) * Cn);
-    uint8_t *used = malloc(Cn);
-    double best = -1.0;
-    uint64_t u = 0;
-    for (uint32_t rd = 0; rd < rounds; rd++) {
-        uint32_t cnt = 0;
-        for (uint32_t l = 0; l < leaves; l++) {
-            int v = 0;
-            memset(used, 0, Cn);
-            for (;;) {                                           /* S4 / S5 */
-                snode *nd = &T[v];
-                if ((uint32_t)nd->depth == Cn) break;
-                if ((uint32_t)nd->nch < Cn - nd->depth) {
-                    uint32_t c, seen = 0;
-                    for (c = 0; c < Cn; c++) { if (used[c]) continue; if (seen++ == (uint32_t)nd->nch) break; }
-                    int id = (int)nn++;
-                    T[id].parent = v; T[id].cls = (int)c; T[id].depth = nd->depth + 1;
-                    if (nd->nch == nd->cap) { nd->cap = nd->cap ? 2 * nd->cap : 4; nd->ch = realloc(nd->ch, sizeof(int) * nd->cap); }
-                    nd->ch[nd->nch++] = id;
-                    used[c] = 1;
-                    v = id;
-                    break;
-                }
-                double Nx = (double)(nd->N + nd->vl), bu = -1.0;
-                int bc = -1;
-                for (int x = 0; x < nd->nch; x++) {
-                    snode *cn = &T[nd->ch[x]];
-                    double Nv = (double)(cn->N + cn->vl);
-                    double ucb = pow(cn->s, alpha) + beta * sqrt(log(Nx) / Nv);
-                    if (ucb > bu) { bu = ucb; bc = nd->ch[x]; }
-                }
-                used[T[bc].cls] = 1;
-                v = bc;
-            }
-            for (int x = v; x >= 0; x = T[x].parent) T[x].vl++;
-            leaf[l] = v;
-            uint32_t d = (uint32_t)T[v].depth;
-            for (int x = v; x > 0; x = T[x].parent) seq[T[x].depth - 1] = (uint32_t)T[x].cls;
-            uint32_t trials = d == Cn ? 1 : rollouts;
-            for (uint32_t tr = 0; tr < trials; tr++) {
-                uint32_t nr = 0;
-                for (uint32_t c = 0; c < Cn; c++) {
-                    int on = 0;
-                    for (uint32_t p = 0; p < d; p++) if (seq[p] == c) on = 1;
-                    if (!on) rest[nr++] = c;
-                }
-                uint64_t rs = smix(seed ^ smix(u + 0x51A9u));
-                for (uint32_t x = nr; x > 1; x--) {
-                    rs += 0x9E3779B97F4A7C15ull;
-                    uint32_t y = (uint32_t)(smix(rs) % x), t2 = rest[x - 1];
-                    rest[x - 1] = rest[y]; rest[y] = t2;
-                }
-                for (uint32_t x = 0; x < nr; x++) seq[d + x] = rest[x];
-                for (uint32_t p = 0; p < Cn; p++) prio[seq[p]] = Cn - 1 - p;
-                memcpy(spl + (size_t)cnt * m * nm, split, m * nm);
-                nn_[cnt] = n;
-                s_order(pb, split, base, clsof, C, Cn, prio, 0, n_max, fw + (size_t)cnt * n_max);
-                s_order(pb, split, base, clsof, C, Cn, prio, 1, n_max, bw + (size_t)cnt * n_max);
-                owner[cnt] = (int)l;
-                cnt++;
-                u++;
-            }
-        }
-        /* S3: score every rollout of the round */
-        ocands cs = {n_max, fbw, spl, nn_, fw, bw, fb};
-        double *lb = calloc(leaves, sizeof(double));
-        for (uint32_t x = 0; x < cnt; x++) {
-            ores r;
-            interleave_one(pb, &cs, x, bits + (size_t)x * P * fbw, &r, NULL);
-            if (n_strat) {                                  /* then per-layer memory opt. (M1-M4) */
-                ocands c1 = {n_max, fbw, spl + (size_t)x * m * nm, nn_ + x, fw + (size_t)x * n_max,
-                             bw + (size_t)x * n_max, bits + (size_t)x * P * fbw};
-                uint8_t *sel = malloc((size_t)P * 2 * n_max);
-                memopt_one(pb, &mn, &c1, 0, sel, &r, NULL, NULL);
-                free(sel);
-            }
-            double sc = r.status == ST_OK ? LB / (double)r.makespan : 0.0;
-            if (sc > lb[owner[x]]) lb[owner[x]] = sc;
-            if (sc > best) {
-                best = sc;
-                *best_makespan = r.makespan;
-                if (best_fwd) memcpy(best_fwd, fw + (size_t)x * n_max, sizeof(uint16_t) * n_max);
-                if (best_bwd) memcpy(best_bwd, bw + (size_t)x * n_max, sizeof(uint16_t) * n_max);
-                if (best_bits) memcpy(best_bits, bits + (size_t)x * P * fbw, sizeof(uint32_t) * P * fbw);
-            }
-        }
-        *scored_out += cnt;
-        for (uint32_t l = 0; l < leaves; l++)                       /* S6 */
-            for (int x = leaf[l]; x >= 0; x = T[x].parent) {
-                if (lb[l] > T[x].s) T[x].s = lb[l];
-                T[x].N++;
-                T[x].vl--;
-            }
-        free(lb);
-        if (trace) trace[rd] = best;
-    }
-    *best_score = best > 0.0 ? best : 0.0;
-    if (!(best > 0.0)) *best_makespan = UINT64_MAX;     /* no feasible (status OK) rollout */
-    for (uint32_t x = 0; x < nn; x++) free(T[x].ch);
-    free(T); free(spl); free(nn_); free(fw); free(bw); free(fb); free(bits); free(owner); free(leaf);
-    free(seq); free(prio); free(rest); free(used); free(base); free(clsof);
+    srch_ctx c = {pb, &mn, n_max, fbw, n, C, Cn, split, base, clsof, LB, -1.0, best_makespan, best_fwd, best_bwd, best_ord};
+    mcts_run(Cn, seed, rounds, leaves, rollouts, alpha, beta, search_score, &c, trace, NULL, NULL, NULL, NULL, NULL,
+             scored_out);
+    *best_score = c.best > 0.0 ? c.best : 0.0;
+    if (!(c.best > 0.0)) *best_makespan = UINT64_MAX;     /* no feasible (status OK) rollout */
+    free(base); free(clsof);
     return 0;
 }
 
@@ -1253,16 +1394,19 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
     uint64_t *cl = malloc(sizeof(uint64_t) * 3 * mn->S * n);     /* candidates of each pair */
     uint32_t *nc = malloc(sizeof(uint32_t) * n), *cur = malloc(sizeof(uint32_t) * n);
     uint32_t *sF = malloc(sizeof(uint32_t) * n), *sB = malloc(sizeof(uint32_t) * n), *qpos = malloc(sizeof(uint32_t) * n);
+    uint32_t *fseg = malloc(sizeof(uint32_t) * n);
     for (uint32_t r = 0; r < P; r++) {
         /* the rank's order: slot of the p-th forward and of the q-th backward stage (O5) */
         uint32_t fi = 0, bi = 0;
         uint32_t *slotB_of_seg = malloc(sizeof(uint32_t) * (idmax + 1)), *qpos_of_seg = malloc(sizeof(uint32_t) * (idmax + 1));
+        const uint16_t *ordr = cs->ord ? cs->ord + (x * (uint64_t)P + r) * 2 * n_max : NULL;
         for (uint32_t t = 0; t < 2 * n; t++) {
-            if ((fb[r * fbw + t / 32] >> (t % 32)) & 1u) { slotB_of_seg[bwd[bi]] = t; qpos_of_seg[bwd[bi]] = bi; bi++; }
-            else { sF[fi] = t; fi++; }
+            uint32_t isb = ordr ? (uint32_t)(ordr[t] >> 15) : ((fb[r * fbw + t / 32] >> (t % 32)) & 1u);
+            if (isb) { uint32_t sg = ordr ? (ordr[t] & 0x7FFFu) : bwd[bi]; slotB_of_seg[sg] = t; qpos_of_seg[sg] = bi; bi++; }
+            else { fseg[fi] = ordr ? (ordr[t] & 0x7FFFu) : fwd[fi]; sF[fi] = t; fi++; }
         }
-        for (uint32_t p = 0; p < n; p++) {                          /* pair p = segment fwd[p] */
-            uint32_t s = fwd[p], i = si[s], lay = layers_of(pb, i, sk[s] * P + r), toff = pb->tab_off[i] + W[s];
+        for (uint32_t p = 0; p < n; p++) {                          /* pair p = the p-th forward stage */
+            uint32_t s = fseg[p], i = si[s], lay = layers_of(pb, i, sk[s] * P + r), toff = pb->tab_off[i] + W[s];
             uint32_t ff[8], bb[8], aa[8];
             for (uint32_t c = 0; c < mn->n_strat; c++) {
                 ff[c] = mn->f[c * T + toff]; bb[c] = mn->b[c * T + toff]; aa[c] = mn->act[c * T + toff];
@@ -1278,7 +1422,7 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
                            rstats ? rstats + 5 * (size_t)r : NULL);
         for (uint32_t p = 0; p < n; p++) {
             const uint64_t *a = cl + (size_t)3 * mn->S * p + 3 * cur[p];
-            uint64_t *o = ovr + ((uint64_t)r * (idmax + 1) + fwd[p]) * 3;
+            uint64_t *o = ovr + ((uint64_t)r * (idmax + 1) + fseg[p]) * 3;
             o[0] = a[0]; o[1] = a[1]; o[2] = a[2];
             sel[((size_t)r * 2 + 0) * n_max + p] = (uint8_t)cur[p];
             sel[((size_t)r * 2 + 1) * n_max + qpos[p]] = (uint8_t)cur[p];
@@ -1287,7 +1431,7 @@ static void memopt_one(const oproblem *pb, const omenu *mn, const ocands *cs, ui
     }
     eval_one(pb, cs, x, res, peaks, NULL, NULL, ovr);          /* M4 */
     free(base); free(W); free(si); free(sk); free(ovr); free(cl); free(nc); free(cur);
-    free(sF); free(sB); free(qpos);
+    free(sF); free(sB); free(qpos); free(fseg);
 }
 
 typedef struct {

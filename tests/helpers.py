@@ -142,3 +142,18 @@ def diamond_problem(P: int = 4, m: int = 6, seed: int = 0) -> Problem:
             off.append(len(units))
     return Problem("diamond", P, m, mods, np.array(off, np.uint32), np.array(units, np.uint16),
                    np.full(P, 700, np.uint32))
+
+
+def orders_array(pb: Problem, rank_orders: List[List[Tuple[str, int]]]) -> np.ndarray:
+    """[P, 2 n_max] u16 per-rank orders (segment id | 0x8000 for backward, 0xFFFF padding) from
+    lists of ('F'|'B', segment id) -- the f1 output format."""
+    out = np.full((pb.P, 2 * pb.n_max), 0xFFFF, np.uint16)
+    for r, seq in enumerate(rank_orders):
+        for t, (d, s) in enumerate(seq):
+            out[r, t] = s | (0x8000 if d == "B" else 0)
+    return out
+
+
+def orders_lists(ords: np.ndarray) -> List[List[Tuple[str, int]]]:
+    """inverse of orders_array for one candidate"""
+    return [[("B" if v & 0x8000 else "F", int(v) & 0x7FFF) for v in row if v != 0xFFFF] for row in ords]

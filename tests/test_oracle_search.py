@@ -5,7 +5,12 @@
   independent priority -> queue-order builder and the (pinned) oracle interleaving;
 * the best-so-far trace never decreases (S:469);
 * the reported best schedule re-scores to the reported makespan with the fixed-order oracle;
-* determinism for a seed.
+* determinism for a seed;
+* the tree policy alone (S4-S6), scored by a table over the first class of a sequence
+  (so the random completions do not matter), against hand-worked traces: every node's (parent,
+  class, N, s) after 9 single-leaf rounds with alpha = 2, beta = 0.5 (the UCB values of every
+  selection are written out below), and after 5 two-leaf rounds (virtual visits, R-35). Swapping
+  ln N_x and N_v, ignoring alpha, or selecting before every child exists changes these trees.
 """
 import itertools
 
@@ -78,7 +83,7 @@ def brute_force(pb, split):
         cs.n[x] = n
         cs.fwd[x, :n] = f
         cs.bwd[x, :n] = b
-    bits, r = oracle.interleave(pb, cs, threads=8)
+    ords, r = oracle.interleave(pb, cs, threads=8)
     md = pb.modules[0]                       # one module, L divisible by P: L / P layers per rank
     LB = (md.L // pb.P) * sum(int(md.f_ns[u]) + int(md.b_ns[u]) for u in pb.inst_units)
     ok = r.status == oracle.ST_OK
@@ -104,8 +109,7 @@ def test_trace_monotone_and_best_record_rescores():
     n = int(c.n[0])
     c.fwd[0] = r["fwd"]
     c.bwd[0] = r["bwd"]
-    c.fb[0] = r["bits"]
-    rr = oracle.evaluate(pb, c)
+    rr = oracle.evaluate(pb, c, orders=r["orders"][None])
     assert rr.status[0] == oracle.ST_OK and int(rr.makespan[0]) == r["makespan"]
     assert sorted(r["fwd"][:n].tolist()) == sorted(cs.fwd[0][:n].tolist())
 
@@ -116,7 +120,7 @@ def test_search_is_deterministic_per_seed():
     a = oracle.search(pb, cs.split[0], seed=5, rounds=10, leaves=3, rollouts=4)
     b = oracle.search(pb, cs.split[0], seed=5, rounds=10, leaves=3, rollouts=4)
     assert np.array_equal(a["trace"], b["trace"]) and a["makespan"] == b["makespan"]
-    assert np.array_equal(a["bits"], b["bits"])
+    assert np.array_equal(a["orders"], b["orders"])
 
 
 def test_exhaustive_budget_with_chunk_classes():
@@ -146,8 +150,57 @@ def test_search_with_memopt_rescores_and_improves_scores():
     c = cs.subset([0])
     c.fwd[0] = b["fwd"]
     c.bwd[0] = b["bwd"]
-    c.fb[0] = b["bits"]
-    sel, rr = oracle.memopt(pb, c, menu, S=10)
+    sel, rr = oracle.memopt(pb, c, menu, S=10, orders=b["orders"][None])
     assert rr.status[0] == oracle.ST_OK and int(rr.makespan[0]) == b["makespan"]
     assert (np.diff(b["trace"]) >= 0).all()
     assert b["trace"][0] >= a["trace"][0] > 0
+
+
+def _tree(t):
+    return [(int(p), int(c), int(n), round(float(v), 4)) for p, c, n, v in zip(t["parent"], t["cls"], t["N"], t["s"])]
+
+
+def test_tree_policy_hand_worked_single_leaf():
+    """Cn = 3 classes, rollout score = a[first class] with a = (0.5, 0.8, 0.72); alpha = 2, beta =
+    0.5, one leaf per round. Rounds 1-3 expand the root's children (0), (1), (2) (unvisited children
+    first). Then UCB = s^2 + 0.5 sqrt(ln N_x / N_v):
+      r4  root N=3: (0) .25+.5241=.7741  (1) .64+.5241=1.1641  (2) .5184+.5241=1.0425 -> (1), expand (1,0)
+      r5  root N=4: .8387, .64+.4163=1.0563, .5184+.5887=1.1071 -> (2), expand (2,0)
+      r6  root N=5: .8843, .64+.4485=1.0885, .5184+.4485=.9669 -> (1), expand (1,2)
+      r7  root N=6: .9193, .64+.3864=1.0264, .9917 -> (1) [full]: (1,0) and (1,2) both 1.1641, tie
+          -> the first, (1,0); expand (1,0,2)
+      r8  root N=7: .9475, .9887, .5184+.4932=1.0116 -> (2), expand (2,1)
+      r9  root N=8: .9710, .64+.3605=1.0005, .9347 -> (1): (1,0) N=2 1.0563, (1,2) N=1 1.2287 -> (1,2),
+          expand (1,2,0)
+    Backpropagation: s = max, N + 1 along the path."""
+    t = oracle.mcts_table(3, seed=1, rounds=9, leaves=1, rollouts=3, alpha=2.0, beta=0.5,
+                          table=[[0.5] * 3, [0.8] * 3, [0.72] * 3])
+    assert _tree(t) == [(-1, -1, 9, 0.8), (0, 0, 1, 0.5), (0, 1, 5, 0.8), (0, 2, 3, 0.72), (2, 0, 2, 0.8),
+                        (3, 0, 1, 0.72), (2, 2, 2, 0.8), (4, 2, 1, 0.8), (3, 1, 1, 0.72), (6, 0, 1, 0.8)]
+    assert t["leaves"][:, 0].tolist() == list(range(1, 10))
+    assert t["trace"].tolist() == [0.5] + [0.8] * 8
+
+
+def test_tree_policy_hand_worked_two_leaves():
+    """the same scores, two leaves per round: the first leaf's path carries a virtual visit while
+    the second is selected (R-35), so a just-expanded child has N_v = 1 and s = 0 until the round
+    is scored (worked with the same UCB as above)"""
+    t = oracle.mcts_table(3, seed=1, rounds=5, leaves=2, rollouts=3, alpha=2.0, beta=0.5,
+                          table=[[0.5] * 3, [0.8] * 3, [0.72] * 3])
+    assert _tree(t) == [(-1, -1, 10, 0.8), (0, 0, 2, 0.5), (0, 1, 5, 0.8), (0, 2, 3, 0.72), (2, 0, 2, 0.8),
+                        (3, 0, 1, 0.72), (2, 2, 2, 0.8), (4, 2, 1, 0.8), (3, 1, 1, 0.72), (6, 0, 1, 0.8),
+                        (1, 1, 1, 0.5)]
+
+
+def test_tree_policy_deeper_scores():
+    """scores that depend on the first two classes, every completion of a depth-2 prefix scoring the
+    same: table[a][b]; the best complete order (2, 0, 1) = 0.9 is found and the root's s is the
+    maximum over the table entries reachable"""
+    tab = [[0.1, 0.1, 0.2], [0.3, 0.3, 0.4], [0.9, 0.5, 0.5]]
+    t = oracle.mcts_table(3, seed=4, rounds=40, leaves=1, rollouts=1, alpha=1.0, beta=0.3, table=tab)
+    assert t["trace"][-1] == 0.9 and (np.diff(t["trace"]) >= 0).all()
+    # every node's s is the best score seen below it: a node's s >= each child's s
+    tr = _tree(t)
+    for x, (p, c, n, v) in enumerate(tr):
+        if p >= 0:
+            assert tr[p][3] >= v and tr[p][2] >= n
