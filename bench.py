@@ -300,23 +300,25 @@ def main():
     try:
         if args.f1_count > 0:
             cnt = min(per, args.f1_count)
-            d_f1 = d_rec[: cnt * model.stride].clone()
+            d_f1 = d_rec[: cnt * model.stride]
             r_f1 = torch.empty(cnt * 24, dtype=torch.uint8, device=dev)
+            o_f1 = torch.empty((cnt, pb.P, 2 * pb.n_max), dtype=torch.int16, device=dev)   # the built orders
             for _ in range(2):
-                dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
+                dip.interleave(model, ws, d_f1, cnt, r_f1, None, d_orders=o_f1, stream=stream)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             reps = max(1, min(args.steps, 5))
             a.record(stream)
             for _ in range(reps):
-                dip.interleave(model, ws, d_f1, cnt, r_f1, None, stream=stream)
+                dip.interleave(model, ws, d_f1, cnt, r_f1, None, d_orders=o_f1, stream=stream)
             b.record(stream)
             torch.cuda.synchronize()
             tf1 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(tf1, op=dist.ReduceOp.MAX)
-            f1 = {"what": "dip_interleave: build each candidate's F/B interleaving with the paper's dual-queue "
-                          "greedy (P:511-548) from its split + priority orders, then score it",
+            f1 = {"what": "dip_interleave: build each candidate's per-rank stage orders with the paper's dual-queue "
+                          "greedy (P:511-548, priority queues over ready stages) from its split + priority orders, "
+                          "emit the orders and score them",
                   "value": cnt * world * reps / (float(tf1[0]) / 1e3), "unit": "candidates/s",
                   "candidates_per_gpu": cnt, "ms_per_call": float(tf1[0]) / reps}
             if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -326,7 +328,7 @@ def main():
                 oracle.interleave(pb, sub, threads=os.cpu_count() or 1)
                 f1["cpu_oracle"] = {"value": sub.count / (time.perf_counter() - t0), "unit": UNIT,
                                     "cores": os.cpu_count() or 1, "sample": f"first {sub.count} candidates"}
-            del d_f1, r_f1
+            del r_f1, o_f1
     except Exception as ex:   # a side measurement must not cost the headline line
         f1 = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 

@@ -163,16 +163,32 @@ dip_status dip_timeline(const dip_model *m, dip_workspace *w, const void *d_reco
                         dip_result *d_results, uint64_t *d_start, uint64_t *d_end, void *stream);
 
 /* DIP's greedy dual-queue stage interleaving (§5.2):
- * for every record, take its split and its forward / backward segment orders as the priority
- * orders of the per-rank queues, build each rank's F/B interleaving with the paper's iterative
- * scheduling (rank with the smallest t_min, 1F1B alternation when both heads are ready before
- * t_last, else the smaller t_start; forward queue disabled while the next forward would exceed
- * the rank's budget), and score the result. The records' F/B bit rows are OVERWRITTEN in place
- * with the built interleaving (zero for BAD_ENCODING; a DEADLOCK keeps the partial rows), so
- * dip_eval_schedules on the same records reproduces d_results exactly. The fused argmin key is
- * updated as by dip_eval_schedules (dip_argmin works after it). Asynchronous on `stream`. */
-dip_status dip_interleave(const dip_model *m, dip_workspace *w, void *d_records, size_t count,
-                          dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+ * for every record, take its split and its forward / backward segment orders as the PRIORITY
+ * orders of the per-rank queues (position 0 = highest; its F/B bit rows are ignored) and build each
+ * rank's stage order with the paper's iterative scheduling (R-29..R-31): a stage is
+ * ready once its predecessors are placed, t_fw / t_bw = the minimum t_start over a queue's ready
+ * stages, the rank with the smallest t_min places one stage -- 1F1B alternation when both are
+ * below t_last, else the queue of the smaller t_start (ties to the backward) -- namely that queue's
+ * highest-priority stage among those starting as early as possible; a forward stage whose
+ * activation would exceed the rank's budget is disabled, and if every rank is blocked
+ * by that alone the gate is lifted for one step (OOM). Scores the built schedule (d_results,
+ * d_peaks_kib as dip_eval_schedules; never DEADLOCK) and updates the fused argmin key
+ * (dip_argmin works after it). d_orders: device [count][P][2*n_max] u16 out, or NULL: rank r's
+ * t-th stage = segment id | 0x8000 for a backward stage, 0xFFFF beyond 2n (all 0xFFFF for
+ * BAD_ENCODING records). The records are not modified. Asynchronous on `stream`. */
+dip_status dip_interleave(const dip_model *m, dip_workspace *w, const void *d_records, size_t count,
+                          dip_result *d_results, uint32_t *d_peaks_kib, uint16_t *d_orders, void *stream);
+
+/* Score schedules given as explicit per-rank orders (the format dip_interleave emits) instead of
+ * the records' shared sequences + F/B bits: the longest path over the stage DAG with
+ * the records' splits, O1-O10 semantics (BAD_ENCODING unless every rank's order holds each present
+ * segment once as F and once as B, 0xFFFF padding; DEADLOCK iff the orders close a cycle).
+ * d_sel (or NULL): a dip_memopt selection [count][P][2][n_max] whose candidates replace the tables'
+ * latencies and activations (f3's re-timing). d_start / d_end (both or neither): device
+ * [count][P][2*n_max] u64 per-slot start / end times (f4). Asynchronous on `stream`. */
+dip_status dip_eval_orders(const dip_model *m, dip_workspace *w, const void *d_records, const uint16_t *d_orders,
+                           size_t count, const uint8_t *d_sel, dip_result *d_results, uint32_t *d_peaks_kib,
+                           uint64_t *d_start, uint64_t *d_end, void *stream);
 
 /* DIP's per-layer memory optimisation (§5.3).
  *
@@ -205,12 +221,14 @@ dip_status dip_strategy_candidates(const dip_model *m, uint32_t module, uint32_t
  * it covers stays within the budget; a Lagrangian bound (R-39) certifies it, else a
  * depth-first branch and bound improves it (at most node_cap children per rank). Then the schedules
  * are scored with the selected latencies and activations (results / peaks / fused argmin key as
- * dip_eval_schedules). d_sel: device
+ * dip_eval_schedules). d_orders: NULL (the records' shared sequences + F/B bits define each rank's
+ * order) or device [count][P][2*n_max] explicit per-rank orders as dip_interleave emits them (then
+ * the re-timing is dip_eval_orders with the selection). d_sel: device
  * [count][P][2][n_max] u8 out -- sel[c][r][0][p] = candidate of the pair whose forward is the
  * p-th forward stage, sel[c][r][1][q] = the same for the q-th backward stage (zero beyond n;
  * unspecified for BAD_ENCODING records). Two launches on `stream`, asynchronous. */
-dip_status dip_memopt(const dip_model *m, dip_workspace *w, const void *d_records, size_t count, uint8_t *d_sel,
-                      dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
+dip_status dip_memopt(const dip_model *m, dip_workspace *w, const void *d_records, const uint16_t *d_orders,
+                      size_t count, uint8_t *d_sel, dip_result *d_results, uint32_t *d_peaks_kib, void *stream);
 
 /* The per-rank ILP solver's settings for dip_memopt: relative optimality gap in per mille
  * (default 50 = the paper's 5 %, 0 = exact) and the branch-and-bound child budget per (record, rank)
@@ -231,7 +249,8 @@ dip_status dip_memopt_stats(const dip_workspace *w, uint64_t *out, void *stream)
  * interleaving -> score LB / makespan (0 if not OK; LB = busiest rank's total latency). Each
  * round selects `leaves` leaves by UCB s^alpha + beta*sqrt(ln N_parent / N_child) with
  * virtual visits, expands one child each (next class in order), scores `rollouts` random
- * completions per leaf in one dip_interleave launch and backpropagates the best trial
+ * completions per leaf in one dip_interleave launch (then dip_memopt on the built orders if
+ * memopt is set) and backpropagates the best trial
  * (s = max, N + 1). Deterministic for a seed (rollout u draws from splitmix64(seed, u)).
  * Allocates its rollout buffers for the duration of the call. Synchronous. */
 typedef struct {
@@ -254,11 +273,13 @@ typedef struct {
     uint64_t tree_nodes;
 } dip_search_result;
 
-/* best_record_out: host buffer of record_stride bytes receiving the best schedule (split, priority
- * orders and its interleaved F/B bits), or NULL; trace: [rounds] best score after each round, or NULL. */
+/* best_record_out: host buffer of record_stride bytes receiving the best rollout's record (split and
+ * priority orders; its F/B bit rows are not meaningful), or NULL; best_orders_out: host
+ * [P][2*n_max] u16 receiving the best rollout's per-rank orders as dip_interleave emits them, or
+ * NULL; trace: [rounds] best score after each round, or NULL. */
 dip_status dip_search(const dip_model *m, dip_workspace *w, const uint8_t *split /* [m*n_modules] */,
-                      const dip_search_params *p, void *best_record_out, double *trace,
-                      dip_search_result *out, void *stream);
+                      const dip_search_params *p, void *best_record_out, uint16_t *best_orders_out,
+                      double *trace, dip_search_result *out, void *stream);
 
 typedef struct {
     int32_t found;            /* 0 if no candidate has status OK on any rank */
@@ -296,8 +317,10 @@ dip_status dip_eval_host(const dip_model *m, dip_workspace *w, const void *h_rec
  * after the consumer's last stage that ends no later than the producer starts (so every receive is
  * posted before its send in simulated time) and wait_irecv right before the consuming stage;
  * consecutive isend / irecv actions share a batch id ("grouped into a batched operation").
- * record: one host record (as encoded / interleaved); start / end: its host timeline rows
- * ([P][2*n_max], from dip_timeline). actions: capacity entries, rank r's list is
+ * record: one host record (as encoded); orders: NULL (the record's shared sequences + F/B bits give
+ * each rank's order) or the schedule's host per-rank orders [P][2*n_max] as dip_interleave emits
+ * them; start / end: its host timeline rows ([P][2*n_max], from dip_timeline or dip_eval_orders).
+ * DIP_EINVAL for a malformed record / orders (a segment missing or repeated on a rank). actions: capacity entries, rank r's list is
  * actions[rank_off[r] .. rank_off[r+1]). DIP_ERANGE if capacity is too small (rank_off[P] = size). */
 enum { DIP_ACT_FW_STAGE = 0, DIP_ACT_BW_STAGE = 1, DIP_ACT_ISEND = 2, DIP_ACT_IRECV = 3,
        DIP_ACT_WAIT_ISEND = 4, DIP_ACT_WAIT_IRECV = 5 };
@@ -308,13 +331,13 @@ typedef struct {
     uint32_t batch;           /* P2P: batch id (consecutive P2P actions share one); stages: 0 */
     uint32_t slot;            /* the stage slot the action belongs to */
 } dip_action;
-dip_status dip_compile_plan(const dip_model *m, const void *record, const uint64_t *start, const uint64_t *end,
-                            dip_action *actions, size_t capacity, uint32_t *rank_off /* [P+1] */,
-                            uint32_t *n_messages);
+dip_status dip_compile_plan(const dip_model *m, const void *record, const uint16_t *orders,
+                            const uint64_t *start, const uint64_t *end, dip_action *actions, size_t capacity,
+                            uint32_t *rank_off /* [P+1] */, uint32_t *n_messages);
 /* Discrete-event execution of a plan (P2P priced as on the schedule's edges): *ok = 1 iff every
  * isend / irecv tag is perfectly paired and the plan terminates; stage_start ([P][2*n_max], or
  * NULL) receives each stage's start time, which equals the source timeline for compiled plans. */
-dip_status dip_validate_plan(const dip_model *m, const void *record, const dip_action *actions,
+dip_status dip_validate_plan(const dip_model *m, const void *record, const uint16_t *orders, const dip_action *actions,
                              const uint32_t *rank_off, uint64_t *stage_start, int32_t *ok);
 
 /* NCCL communicator for the argmin: rank 0 calls dip_comm_unique_id, broadcasts

@@ -260,6 +260,21 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     kp.g_ring = gput(2 * P * dipk::RING_D * 8);
     kp.g_bmf = gput(3 * m * nm);
     kp.g_bytes = go;
+    // per-rank-order kernel (f1 build / explicit-order timing): per-segment cost rows, priority
+    // orders and their inverses, per-segment F / B slots, ranks-done counters, per-rank ready bitmaps
+    {
+        uint32_t oo = 0;
+        auto oput = [&](uint32_t bytes) { const uint32_t o = oo; oo = up16(oo + bytes); return o; };
+        const uint32_t nwd = (n_max + 31) / 32;
+        kp.o_row = oput(4 * n_max);
+        kp.o_seq = oput(2 * 2 * M->n_pad);
+        kp.o_posof = oput(2 * 2 * n_max);
+        kp.o_sl = oput(2 * 8 * n_max);
+        kp.o_h = oput(2 * n_max);
+        kp.o_bm = oput(2 * 4 * P * nwd);
+        kp.o_mb = oput(3 * m * nm);
+        kp.o_bytes = oo;
+    }
 
     if (cuda_device < 0) {   // host-only model: encoding and validation, no device resources
         *out = guard.release();
@@ -289,6 +304,25 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     M->smem = best_smem;
     M->grid = M->num_sms * best_bps;
     CUDA_TRY(dipk::prepare_eval(G, best_smem));
+    {   // the per-rank-order kernel's shape
+        const size_t per_warp_o = (size_t)M->cpg * kp.o_bytes;
+        int bw = 0, bwpb = 0, bbps = 0;
+        size_t bsm = 0;
+        for (int wpb = 1; wpb <= 8; wpb++) {
+            const size_t sm = kp.blob_bytes + wpb * per_warp_o;
+            if (sm > smem_cap) break;
+            CUDA_TRY(dipk::prepare_order(G, sm));
+            int bps = 0;
+            CUDA_TRY(dipk::occupancy_order(G, wpb * 32, sm, &bps));
+            if (bps < 1) continue;
+            if (wpb * bps >= bw) { bw = wpb * bps; bwpb = wpb; bbps = bps; bsm = sm; }
+        }
+        if (!bw) return fail(DIP_ERANGE, "per-schedule order working set does not fit in shared memory");
+        M->o_wpb = bwpb;
+        M->o_smem = bsm;
+        M->o_grid = M->num_sms * bbps;
+        CUDA_TRY(dipk::prepare_order(G, bsm));
+    }
 
     CUDA_TRY(cudaMalloc(&M->d_blob, kp.blob_bytes));
     CUDA_TRY(cudaMemcpy(M->d_blob, blob.data(), kp.blob_bytes, cudaMemcpyHostToDevice));
@@ -478,11 +512,11 @@ dip_status dip_eval_schedules(const dip_model *M, dip_workspace *w, const void *
     return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s);
 }
 
-dip_status dip_interleave(const dip_model *M, dip_workspace *w, void *d_records, size_t count, dip_result *d_results,
-                          uint32_t *d_peaks, void *stream) {
-    if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
-    if (count && (!d_records || !d_results)) return fail(DIP_EINVAL, "null buffer");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+// the per-rank-order kernel: BUILD (f1) or TIME (explicit orders, optional f3 selection / timelines)
+static dip_status launch_orders(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
+                                bool build, const uint16_t *orders_in, uint16_t *orders_out, const uint8_t *sel,
+                                dip_result *d_results, uint32_t *d_peaks, uint64_t *d_start, uint64_t *d_end,
+                                cudaStream_t s) {
     const uint32_t idx_bits = bits_for(std::max<uint64_t>(count, 2));
     const bool fused = fused_ok(M, idx_bits);
     CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
@@ -491,8 +525,54 @@ dip_status dip_interleave(const dip_model *M, dip_workspace *w, void *d_records,
     w->last_idx_bits = idx_bits;
     w->last_fused = fused;
     if (!count) return DIP_OK;
-    return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s,
-                        static_cast<uint8_t *>(d_records));
+    KParams kp = M->kp;
+    kp.records = static_cast<const uint8_t *>(d_records);
+    kp.records_out = nullptr;
+    kp.orders_out = orders_out;
+    kp.orders_in = orders_in;
+    kp.sel = sel;
+    kp.tl_start = d_start;
+    kp.tl_end = d_end;
+    kp.count = count;
+    kp.index_base = 0;
+    kp.results = d_results;
+    kp.peaks = d_peaks;
+    kp.counter = w->d_misc + 0;
+    kp.best_key = w->d_misc + 1;
+    kp.spill = nullptr;
+    kp.fused_key = fused ? 1u : 0u;
+    kp.idx_bits = idx_bits;
+    CUDA_TRY(cudaMemsetAsync(kp.counter, 0, sizeof(unsigned long long), s));
+    if (d_start) {
+        CUDA_TRY(cudaMemsetAsync(d_start, 0, count * M->P * 2ull * M->n_max * 8, s));
+        CUDA_TRY(cudaMemsetAsync(d_end, 0, count * M->P * 2ull * M->n_max * 8, s));
+    }
+    const int grid = (int)std::min<uint64_t>((uint64_t)M->o_grid,
+                                             std::max<uint64_t>(1, (count + M->cpg * M->o_wpb - 1) / (M->cpg * M->o_wpb)));
+    CUDA_TRY(dipk::launch_order(kp, M->G, build, grid, M->o_wpb * 32, M->o_smem, s));
+    g_launches++;
+    return DIP_OK;
+}
+
+dip_status dip_interleave(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
+                          dip_result *d_results, uint32_t *d_peaks, uint16_t *d_orders, void *stream) {
+    if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
+    if (count && (!d_records || !d_results)) return fail(DIP_EINVAL, "null buffer");
+    if (M->device < 0 || !M->d_blob) return fail(DIP_EINVAL, "host-only model (cuda_device < 0)");
+    return launch_orders(M, w, d_records, count, true, nullptr, d_orders, nullptr, d_results, d_peaks, nullptr,
+                         nullptr, static_cast<cudaStream_t>(stream));
+}
+
+dip_status dip_eval_orders(const dip_model *M, dip_workspace *w, const void *d_records, const uint16_t *d_orders,
+                           size_t count, const uint8_t *d_sel, dip_result *d_results, uint32_t *d_peaks,
+                           uint64_t *d_start, uint64_t *d_end, void *stream) {
+    if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
+    if (count && (!d_records || !d_orders || !d_results)) return fail(DIP_EINVAL, "null buffer");
+    if (!d_start != !d_end) return fail(DIP_EINVAL, "d_start and d_end go together");
+    if (d_sel && !M->S) return fail(DIP_EINVAL, "a selection needs a strategy menu (dip_set_strategies)");
+    if (M->device < 0 || !M->d_blob) return fail(DIP_EINVAL, "host-only model (cuda_device < 0)");
+    return launch_orders(M, w, d_records, count, false, d_orders, nullptr, d_sel, d_results, d_peaks, d_start, d_end,
+                         static_cast<cudaStream_t>(stream));
 }
 
 dip_status dip_timeline(const dip_model *M, dip_workspace *w, const void *d_records, size_t count, dip_result *d_results,
@@ -656,6 +736,9 @@ dip_status dip_eval_host(const dip_model *M, dip_workspace *w, const void *h_rec
     const size_t nch = (count + C - 1) / C;
     CUDA_TRY(cudaEventRecord(w->ev_start, s));              // comp2 starts after the key reset
     CUDA_TRY(cudaStreamWaitEvent(w->comp2, w->ev_start, 0));
+    // the copies too: work the caller queued on `s` before this call (e.g. an asynchronous fill of
+    // the pinned h_records) must complete before the first chunk is read
+    CUDA_TRY(cudaStreamWaitEvent(w->copy_stream, w->ev_start, 0));
     for (size_t c = 0; c < nch; c++) {
         const int b = (int)(c % dip_workspace::NBUF);
         const bool odd = (c & 1) != 0;

@@ -55,6 +55,8 @@ struct dip_model {
     dipk::KParams kp{};            // shape + blob + layout; per-launch fields filled per call
     int G = 32, cpg = 1, wpb = 1, bps = 1, grid = 1, num_sms = 148;
     size_t smem = 0;
+    int o_wpb = 1, o_grid = 1;         // per-rank-order kernel (dip_order.cu) shape
+    size_t o_smem = 0;
     uint64_t mk_bound = 0;
     // f3 (per-layer memory optimisation): strategy menu -> candidate table
     uint32_t n_strat = 0, S = 0;

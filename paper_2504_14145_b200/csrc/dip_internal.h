@@ -35,11 +35,15 @@ struct KParams {
     // per-candidate shared-memory working set (byte offsets inside a group area)
     uint32_t g_seqF, g_seqB, g_posF, g_posB, g_depF0, g_depBP, g_ring, g_bmf, g_bytes;
     uint32_t warps_per_block, cpg;
+    // per-schedule working set of the per-rank-order kernel (dip_order.cu), byte offsets in a group area
+    uint32_t o_row, o_seq, o_posof, o_sl, o_h, o_bm, o_mb, o_bytes;
     // per launch
     const uint8_t *records;
     uint8_t *records_out;       // non-null: interleave mode (f1) writes the F/B bit rows here
     uint64_t *tl_start, *tl_end;  // non-null: timeline mode, [count][P][2*n_max] per-slot start / end
     const uint8_t *sel;         // non-null: f3 mode, [count][P][2][n_max] selected candidate per stage pair
+    uint16_t *orders_out;       // order kernel, BUILD: [count][P][2 n_max] per-rank orders out (or null)
+    const uint16_t *orders_in;  // order kernel, TIME: [count][P][2 n_max] per-rank orders in
     const uint4 *ctab;          // f3 candidates {F ns, B ns, act KiB, count} per (type, W, c)
     const int32_t *crow;        // f3: per chunk row, ctab base of its (module, layers) type - tab_off * S
     const uint16_t *srank;      // f3: per ctab entry c, the rank of the step c -> c+1 by saving per KiB
@@ -69,6 +73,9 @@ cudaError_t prepare_memopt(size_t smem);
 cudaError_t occupancy_memopt(size_t smem, int *blocks_per_sm);
 cudaError_t launch_memopt(const KParams &kp, uint8_t *sel, uint32_t warp_bytes, int grid, cudaStream_t s);
 cudaError_t prepare_eval(int G, size_t smem);
+cudaError_t prepare_order(int G, size_t smem);
+cudaError_t occupancy_order(int G, int block, size_t smem, int *blocks_per_sm);
+cudaError_t launch_order(const KParams &kp, int G, bool build, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm);
 cudaError_t launch_scan_argmin(const dip_result *res, uint64_t count, uint64_t index_base,
                                unsigned long long *mk_out, unsigned long long *idx_out, cudaStream_t s);

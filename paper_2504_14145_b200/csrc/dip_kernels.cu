@@ -17,10 +17,10 @@
 // stages ahead of its consumer, so the lock-step wavefront never blocks on a full channel
 // (no false deadlocks: "no lane can progress" <=> the candidate's DAG has a cycle).
 //
-// The same kernel template serves the §8(f) rows: MODE 1 builds each candidate's F/B
-// interleaving with DIP's dual-queue greedy first (f1), MODE 2 also records every
-// stage's start / end (f4's timelines), MODE 3 takes each stage pair's latency and activation
-// from the f3 candidate table through a per-(candidate, rank, position) selection.
+// The same kernel template serves the §8(f) rows on records: MODE 2 also records every stage's
+// start / end (f4's timelines), MODE 3 takes each stage pair's latency and activation from the f3
+// candidate table through a per-(candidate, rank, position) selection. Schedules given
+// as per-rank orders (f1's dual-queue output) run in dip_order.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -128,8 +128,8 @@ __device__ __noinline__ void spill_keep(unsigned long long *spill, uint32_t d, u
     spill[(d ? (P + r) : r) * n_max + idx - RING_D] = v;
 }
 
-// MODE 0: score the given schedules; MODE 1: build them (f1) and score; MODE 2: score and record
-// every stage's start / end (f4); MODE 3: score with each stage pair's selected memory strategy (f3)
+// MODE 0: score the given schedules; MODE 2: score and record every stage's start / end (f4);
+// MODE 3: score with each stage pair's selected memory strategy (f3)
 template <int G, int MODE>
 __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -255,11 +255,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         }
         // F/B bit rows: exactly n ones in [0, 2n), zeros beyond
         uint32_t wcur = 0, wnext = 0;
-        if (MODE == 1 && laneOn && gvalid) {   // the interleaving overwrites the record's F/B bit rows
-            uint32_t *fbo = reinterpret_cast<uint32_t *>(kp.records_out + cand * (uint64_t)kp.stride + kp.off_fb);
-            for (uint32_t w = 0; w < kp.fbw; w++) fbo[w * P + r] = 0u;
-        }
-        if (MODE != 1 && laneOn) {
+        if (laneOn) {
             const uint32_t lim = 2 * n;
             uint32_t ones = 0;
             for (uint32_t w = 0; w < kp.fbw; w++) {
@@ -351,7 +347,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         uint64_t tlast = 0, busy = 0;
         uint32_t cur = 0, peak = 0;
         const uint32_t S2 = 2 * n;
-        if (MODE != 1) {   // MODE 0 / 3: score; MODE 2: score and record every stage's start/end
+        {   // MODE 0 / 3: score; MODE 2: score and record every stage's start/end
         // ---------------- K3: lock-step wavefront longest path ----------------
         // Per round every lane of the group tries its next slot (F if bit t is 0, else B):
         // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
@@ -475,161 +471,6 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             }
         }
 
-        } else {
-        // ---------------- f1: DIP's dual-queue greedy interleaving ----------------
-        // One stage per step per candidate, exactly in the order of the sequential algorithm: every
-        // lane (rank) evaluates the t_start of its two in-order queue heads (the dependency values
-        // come through the same channel rings and wrap slots as the scorer), applies the memory
-        // gate (R-30), the group picks the rank with the smallest t_min (ties to the
-        // lowest rank) and that rank places one stage: alternating F/B when both heads are
-        // ready before t_last, else the smaller t_start (ties to B, R-29). If every rank
-        // is blocked by its gate only, the gate is lifted for one step (R-31).
-        uint32_t fi = 0, bi = 0, wbuf = 0;      // forward / backward stages placed so far
-        int last = -1;
-        bool done = bad || !laneOn || n == 0;
-        uint32_t *fbOut = reinterpret_cast<uint32_t *>(kp.records_out + (gvalid ? cand : 0) * (uint64_t)kp.stride + kp.off_fb) + r;
-        const uint32_t colIn0 = (uint32_t)r - 1, colIn1 = P * D + r + 1;   // producer columns (F, B)
-        const uint32_t colOut0 = (uint32_t)r, colOut1 = P * D + r;         // own columns (F, B)
-        const uint32_t bud = budget[laneOn ? r : 0];
-        // each lane's two queue heads are cached and re-evaluated only when a placement can change
-        // them: the placer's head in the placed direction, its consumer neighbour's head in that
-        // direction, and the wrap consumers (rank 0's F head after rank P-1 places an F, rank P-1's
-        // B head after rank 0 places a B or after rank P-1 places an F -- the loss turnaround)
-        uint2 eF = make_uint2(0u, 0u), eB = make_uint2(0u, 0u);
-        uint4 TF = make_uint4(0u, 0u, 0u, 0u), TB = make_uint4(0u, 0u, 0u, 0u);
-        uint32_t layF = 0, layB = 0;
-        uint64_t tF = 0, tB = 0;
-        bool rdyF = false, rdyB = false, needF = true, needB = true;
-        uint32_t fstep = 0;
-        for (;;) {
-            const uint32_t fu = __shfl_up_sync(FULL, fi, 1, G), bu = __shfl_up_sync(FULL, bi, 1, G);
-            const uint32_t fd = __shfl_down_sync(FULL, fi, 1, G), bd = __shfl_down_sync(FULL, bi, 1, G);
-            if (G < 32 || (__any_sync(FULL, needF) && needF)) {   // forward head
-                const bool hasF = !done && fi < n;
-                eF = hasF ? posAll[fi] : make_uint2(0u, 0u);
-                TF = tab[eF.x & 0xFFFu];
-                layF = layers[((eF.x >> 12) & 0xFFFu) + r];
-                uint64_t vF = hasF ? (isFirst ? depAll[eF.y & 0xFFFFu] : ringAll[(fi & (D - 1)) * P + colIn0]) : 0ull;
-                rdyF = hasF && (isFirst ? (uint32_t)(vF >> 32) < (1u << 24) : fu > fi);
-                if (rdyF && !isFirst && fi + D < fu) vF = spill_load(spill, 0, r, P, n_max, fi);
-                tF = vF + (isFirst ? 0u : TF.w);           // used only when ready (pending byte 0)
-            }
-            if (G < 32 || (__any_sync(FULL, needB) && needB)) {   // backward head
-                const bool hasB = !done && bi < n;
-                eB = hasB ? posAll[n_max + bi] : make_uint2(0u, 0u);
-                TB = tab[eB.x & 0xFFFu];
-                layB = layers[((eB.x >> 12) & 0xFFFu) + r];
-                uint64_t vB = hasB ? (isLast ? depAll[eB.y & 0xFFFFu] : ringAll[(bi & (D - 1)) * P + colIn1]) : 0ull;
-                rdyB = hasB && (isLast ? (uint32_t)(vB >> 32) < (1u << 24) : bd > bi);
-                if (rdyB && !isLast && bi + D < bd) vB = spill_load(spill, 1, r, P, n_max, bi);
-                tB = vB + TB.w;
-            }
-            // memory gate and the group's argmin of (t_min, rank)
-            const uint32_t actF = layF * TF.z;
-            const bool gated = rdyF && cur + actF > bud;
-            const uint64_t INF = ~0ull;
-            const uint64_t kF = (rdyF && !gated) ? tF : INF, kB = rdyB ? tB : INF;
-            const uint64_t tmin = kF < kB ? kF : kB;
-            uint64_t key = tmin == INF ? INF : (tmin << 5) | (uint64_t)r;
-            uint64_t gk = group_min<G>(key);
-            bool relax = false;
-            // (a whole-warp group's gk is warp-uniform: no vote needed)
-            if (G == 32 ? gk == INF : __any_sync(FULL, gk == INF)) {   // stuck only because of gates? (R-31)
-                const uint64_t k2 = rdyF ? ((tF << 5) | (uint64_t)r) : INF;
-                const uint64_t g2 = group_min<G>(k2);      // every lane shuffles; stuck groups use it
-                if (gk == INF) { gk = g2; relax = true; }
-            }
-            // exit / cycle checks (every 8th step for a whole-warp group: a step without a placement
-            // repeats forever, so the verdict is exact; a finished group idles at most 7 steps)
-            if (G < 32 || (++fstep & 7) == 0) {
-                const uint32_t alive = __ballot_sync(FULL, !done);
-                if (alive == 0) break;
-                if (gk == INF && (alive & gmask)) {        // no rank of this group can place a stage: a cycle
-                    dl = true;
-                    done = true;
-                }
-            }
-            __syncwarp();
-            uint32_t pdir = 0;
-            if (!done && gk != INF && (uint32_t)(gk & 31u) == (uint32_t)r) {
-                const bool fOK = rdyF && (!gated || relax);
-                const bool bOK = rdyB;
-                uint32_t dir;
-                if (fOK && bOK && tF < tlast && tB < tlast) dir = last == 0 ? 1u : 0u;   // emulate 1F1B
-                else if (!fOK) dir = 1u;
-                else if (!bOK) dir = 0u;
-                else dir = tB <= tF ? 1u : 0u;
-                // the placement, specialised per direction at compile time (one lane runs it, so the
-                // branch on dir costs nothing and the F / B selects disappear)
-                auto place = [&](auto dirc) {
-                    constexpr uint32_t DIR = decltype(dirc)::value;
-                    const uint2 e = DIR ? eB : eF;
-                    const uint4 T = DIR ? TB : TF;
-                    const uint32_t lay = DIR ? layB : layF;
-                    const uint32_t idx = DIR ? bi : fi;
-                    const uint64_t ts = DIR ? tB : tF;
-                    const uint64_t st = ts > tlast ? ts : tlast;
-                    const uint64_t end = st + (uint64_t)lay * (DIR ? T.y : T.x);
-                    busy += end - st;
-                    tlast = end;
-                    const uint32_t act = lay * T.z;
-                    cur = DIR ? cur - act : cur + act;
-                    peak = cur > peak ? cur : peak;
-                    const bool wrapP = DIR ? isFirst : isLast;
-                    // a plain channel write for interior ranks, the wrap-slot read-modify-write only
-                    // at rank 0 / P-1
-                    if (!wrapP) {
-                        uint64_t *pa = &ringAll[(idx & (D - 1)) * P + (DIR ? colOut1 : colOut0)];
-                        const uint64_t pold = *pa;
-                        *pa = end;
-                        const uint32_t ccnt = DIR ? bu : fd;                 // consumer neighbour's count
-                        if (idx >= ccnt + D) spill_keep(spill, DIR, r, P, n_max, idx, pold);
-                    } else {
-                        uint64_t *pa = &depAll[min(e.y >> 16, SINK)];
-                        const uint64_t pold = *pa;
-                        const int32_t sgn = (int32_t)(e.x << 6) >> 30;
-                        const uint64_t pv = (end + (uint64_t)((int64_t)sgn * (int64_t)T.w)) & VAL_MASK;
-                        const uint64_t cand2 = (pold & HIGH_MASK) | pv;
-                        *pa = (cand2 > pold ? cand2 : pold) + (1ull << PEND_SHIFT);
-                        if (e.x & E_MULTI) {
-                            const uint32_t s = (e.y >> 16) - SINK - 1, dc = segdec[s];
-                            const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7;
-                            const uint32_t msk = DIR ? mi[i].prod_mask : mi[i].cons_mask;
-                            for (uint32_t c = 0; c < nmod; c++) {
-                                if (!((msk >> c) & 1u) || Mb[b * nmod + c] == 0) continue;
-                                uint64_t *sl = &depAll[DIR ? nF + slotB[sbase[b * nmod + c] + mi[c].K - 1] : slotF[sbase[b * nmod + c]]];
-                                const uint64_t old = *sl, c2 = (old & HIGH_MASK) | pv;
-                                *sl = (c2 > old ? c2 : old) + (1ull << PEND_SHIFT);
-                            }
-                        }
-                    }
-                };
-                if (dir) place(std::integral_constant<uint32_t, 1>());
-                else place(std::integral_constant<uint32_t, 0>());
-                const uint32_t t = fi + bi;
-                if (dir) wbuf |= 1u << (t & 31);
-                if ((t & 31) == 31 || t + 1 == S2) { fbOut[(t >> 5) * P] = wbuf; wbuf = 0; }
-                if (dir) bi++; else fi++;
-                last = (int)dir;
-                done = t + 1 == S2;
-                pdir = dir;
-            }
-            // which cached heads the group's placement (if any) may have changed (whole-warp groups
-            // only: with several groups per warp both heads are needed in most steps anyway)
-            if constexpr (G == 32) {
-                const uint32_t pl = (uint32_t)(gk & 31u);
-                const uint32_t dirw = __shfl_sync(FULL, pdir, (int)pl);
-                const bool placed = gk != INF;
-                needF = placed && dirw == 0 && ((uint32_t)r == pl || (uint32_t)r == pl + 1 || (isFirst && pl == P - 1));
-                needB = placed && ((dirw == 1 && ((uint32_t)r == pl || (uint32_t)r + 1 == pl || (isLast && pl == 0))) ||
-                                   (dirw == 0 && isLast && pl == P - 1));
-            }
-            __syncwarp();
-        }
-        if (dl && laneOn && wbuf) {                        // flush the partial word of a deadlocked build
-            const uint32_t t = fi + bi;
-            fbOut[(t >> 5) * P] = wbuf;
-        }
         }
 
         // ---------------- results + K4 argmin ----------------
@@ -709,8 +550,7 @@ __global__ void make_gkey(const unsigned long long *key, unsigned long long *gke
 
 template <int G>
 static cudaError_t launch_g(const KParams &kp, int grid, int block, size_t smem, cudaStream_t s) {
-    if (kp.records_out) dip_eval_kernel<G, 1><<<grid, block, smem, s>>>(kp);
-    else if (kp.tl_start) dip_eval_kernel<G, 2><<<grid, block, smem, s>>>(kp);
+    if (kp.tl_start) dip_eval_kernel<G, 2><<<grid, block, smem, s>>>(kp);
     else if (kp.sel) dip_eval_kernel<G, 3><<<grid, block, smem, s>>>(kp);
     else dip_eval_kernel<G, 0><<<grid, block, smem, s>>>(kp);
     return cudaGetLastError();
@@ -731,19 +571,15 @@ static const void *kfun() { return reinterpret_cast<const void *>(&dip_eval_kern
 static const void *kernel_for(int G, int mode) {
     switch (G * 4 + mode) {
     case 16: return kfun<4, 0>();
-    case 17: return kfun<4, 1>();
     case 18: return kfun<4, 2>();
     case 19: return kfun<4, 3>();
     case 32: return kfun<8, 0>();
-    case 33: return kfun<8, 1>();
     case 34: return kfun<8, 2>();
     case 35: return kfun<8, 3>();
     case 64: return kfun<16, 0>();
-    case 65: return kfun<16, 1>();
     case 66: return kfun<16, 2>();
     case 67: return kfun<16, 3>();
     case 128: return kfun<32, 0>();
-    case 129: return kfun<32, 1>();
     case 130: return kfun<32, 2>();
     case 131: return kfun<32, 3>();
     default: return nullptr;
@@ -752,6 +588,7 @@ static const void *kernel_for(int G, int mode) {
 
 cudaError_t prepare_eval(int G, size_t smem) {
     for (int mode = 0; mode < 4; mode++) {
+        if (mode == 1) continue;   // (mode 1, the old in-order f1, lives in dip_order.cu now)
         const void *f = kernel_for(G, mode);
         if (!f) return cudaErrorInvalidValue;
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -762,7 +599,7 @@ cudaError_t prepare_eval(int G, size_t smem) {
 
 cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm) {
     int best = 1 << 30;
-    for (int mode = 0; mode < 2; mode++) {   // the scorer and f1 set the shape; modes 2, 3 reuse it
+    for (int mode = 0; mode < 1; mode++) {   // the scorer sets the shape; modes 2, 3 reuse it
         const void *f = kernel_for(G, mode);
         if (!f) return cudaErrorInvalidValue;
         int b = 0;

@@ -291,7 +291,36 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(FULL, nsum, o);
         if (nsum != n) bad = true;
         bad = __any_sync(FULL, bad);
-        if (!bad) {
+        const uint16_t *orow = kp.orders_in ? kp.orders_in + (x * P + r) * (uint64_t)(2 * n_max) : nullptr;
+        if (!bad && orow) {
+            // explicit per-rank orders (f1's output): the p-th forward's segment, each segment's
+            // backward position q and the slot of the q-th backward, by warp ballots over the row
+            for (uint32_t p = lane; p < n_max; p += 32) invB[p] = 0xFFFFu;
+            __syncwarp();
+            uint32_t nF = 0, nB = 0;
+            const uint32_t below = (1u << lane) - 1u;
+            for (uint32_t t0 = 0; t0 < 2 * n; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                const uint32_t e = t < 2 * n ? __ldg(&orow[t]) : 0xFFFFu;
+                const bool isB = t < 2 * n && (e & 0x8000u), isF = t < 2 * n && !(e & 0x8000u);
+                const uint32_t bF = __ballot_sync(FULL, isF), bB = __ballot_sync(FULL, isB), sg = e & 0x7FFFu;
+                if (isF) {
+                    const uint32_t p = nF + __popc(bF & below);
+                    if (p < n_max && sg < n_max) fw[p] = (uint16_t)sg;
+                    else bad = true;
+                }
+                if (isB) {
+                    const uint32_t q = nB + __popc(bB & below);
+                    if (q < n_max && sg < n_max) { invB[sg] = (uint16_t)q; bsl[q] = (uint16_t)t; }
+                    else bad = true;
+                }
+                nF += __popc(bF);
+                nB += __popc(bB);
+            }
+            if (nF != n || nB != n) bad = true;
+            bad = __any_sync(FULL, bad);
+            __syncwarp();
+        } else if (!bad) {
             for (uint32_t p = lane; p < n_max; p += 32) {
                 fw[p] = __ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_fwd) + p);
                 invB[p] = 0xFFFFu;
@@ -569,14 +598,38 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
             }
         }
         // the backward row needs each pair's backward position again: rebuild the segment -> position
-        // map from the record into the (now dead) step arrays
-        for (uint32_t q = lane; q < n; q += 32)
-            invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_bwd) + q)] = (uint16_t)q;
-        __syncwarp();
-        for (uint32_t p = lane; p < n_max; p += 32) {
-            const uint8_t c = p < n ? (cn[p] & 15u) : 0;
-            selF[p] = c;
-            if (p < n) selB[invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_fwd) + p)]] = c;
+        // map into the (now dead) step arrays -- from the record's sequences, or from the orders
+        if (orow) {
+            uint16_t *invF = invB;                   // segment -> forward position
+            uint32_t nF = 0, nB = 0;
+            const uint32_t below = (1u << lane) - 1u;
+            for (uint32_t t0 = 0; t0 < 2 * n; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                const uint32_t e = t < 2 * n ? __ldg(&orow[t]) : 0xFFFFu;
+                const bool isF = t < 2 * n && !(e & 0x8000u);
+                const uint32_t bF = __ballot_sync(FULL, isF);
+                if (isF) invF[e & 0x7FFFu] = (uint16_t)(nF + __popc(bF & below));
+                nF += __popc(bF);
+            }
+            __syncwarp();
+            for (uint32_t p = lane; p < n_max; p += 32) selF[p] = p < n ? (cn[p] & 15u) : 0;
+            for (uint32_t t0 = 0; t0 < 2 * n; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                const uint32_t e = t < 2 * n ? __ldg(&orow[t]) : 0xFFFFu;
+                const bool isB = t < 2 * n && (e & 0x8000u);
+                const uint32_t bB = __ballot_sync(FULL, isB);
+                if (isB) selB[nB + __popc(bB & below)] = cn[invF[e & 0x7FFFu]] & 15u;
+                nB += __popc(bB);
+            }
+        } else {
+            for (uint32_t q = lane; q < n; q += 32)
+                invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_bwd) + q)] = (uint16_t)q;
+            __syncwarp();
+            for (uint32_t p = lane; p < n_max; p += 32) {
+                const uint8_t c = p < n ? (cn[p] & 15u) : 0;
+                selF[p] = c;
+                if (p < n) selB[invB[__ldg(reinterpret_cast<const uint16_t *>(rec + kp.off_fwd) + p)]] = c;
+            }
         }
         if (n < n_max)
             for (uint32_t q = n + lane; q < n_max; q += 32) selB[q] = 0;

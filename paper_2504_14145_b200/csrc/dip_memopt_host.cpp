@@ -200,8 +200,8 @@ extern "C" dip_status dip_strategy_candidates(const dip_model *M, uint32_t modul
     return fail(DIP_EINVAL, "no stage pair of this (module, layers)");
 }
 
-extern "C" dip_status dip_memopt(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
-                                 uint8_t *d_sel, dip_result *d_results, uint32_t *d_peaks, void *stream) {
+extern "C" dip_status dip_memopt(const dip_model *M, dip_workspace *w, const void *d_records, const uint16_t *d_orders,
+                                 size_t count, uint8_t *d_sel, dip_result *d_results, uint32_t *d_peaks, void *stream) {
     if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
     if (!M->S) return fail(DIP_EINVAL, "no strategy menu (dip_set_strategies)");
     if (count && (!d_records || !d_results || !d_sel)) return fail(DIP_EINVAL, "null buffer");
@@ -219,11 +219,14 @@ extern "C" dip_status dip_memopt(const dip_model *M, dip_workspace *w, const voi
     kp.count = count;
     kp.counter = w->d_misc + 5;
     kp.mo_stats = w->d_misc + 10;
+    kp.orders_in = d_orders;
     CUDA_TRY(cudaMemsetAsync(w->d_misc + 5, 0, sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(w->d_misc + 10, 0, 5 * sizeof(unsigned long long), s));
     const uint64_t warps = std::min<uint64_t>((uint64_t)M->mo_grid * 4, count * M->P);
     CUDA_TRY(dipk::launch_memopt(kp, d_sel, M->mo_warp_bytes, (int)((warps + 3) / 4), s));
     g_launches++;
+    if (d_orders)   // M4 on explicit orders: the per-rank-order kernel's timing with the selection
+        return dip_eval_orders(M, w, d_records, d_orders, count, d_sel, d_results, d_peaks, nullptr, nullptr, s);
     return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s, nullptr, d_sel);
 }
 

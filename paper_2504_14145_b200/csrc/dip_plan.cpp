@@ -34,8 +34,11 @@ struct Sched {
     std::vector<uint32_t> slotF, slotB;    // [P][n_max] slot of F(s) / B(s) on rank r
 };
 
-// decode one record (host) into per-rank slot lists; returns false if malformed
-bool decode(const dip_model *M, const uint8_t *rec, Sched &S, std::vector<uint8_t> &Mv, std::vector<uint32_t> &W) {
+// decode one record (host) into per-rank slot lists -- each rank's order from the record's shared
+// sequences + F/B bits, or from explicit per-rank orders ([P][2 n_max], dip_interleave's format);
+// returns false if malformed (a segment missing, duplicated or absent from the split on any rank)
+bool decode(const dip_model *M, const uint8_t *rec, const uint16_t *orders, Sched &S, std::vector<uint8_t> &Mv,
+            std::vector<uint32_t> &W) {
     const uint32_t P = M->P, nm = M->nmod, m = M->m;
     uint16_t n16, flags;
     std::memcpy(&n16, rec, 2);
@@ -80,12 +83,26 @@ bool decode(const dip_model *M, const uint8_t *rec, Sched &S, std::vector<uint8_
     S.slotB.assign(P * M->n_max, ~0u);
     for (uint32_t r = 0; r < P; r++) {
         uint32_t fi = 0, bi = 0;
+        if (orders)
+            for (uint32_t t = 2 * n; t < 2 * M->n_max; t++)
+                if (orders[(size_t)r * 2 * M->n_max + t] != 0xFFFFu) return false;
         for (uint32_t t = 0; t < 2 * n; t++) {
-            const uint32_t isb = (fb[(t / 32) * P + r] >> (t % 32)) & 1u;
-            if ((isb ? bi : fi) >= n) return false;
-            const uint32_t s = isb ? bwd[bi++] : fwd[fi++];
+            uint32_t isb, s;
+            if (orders) {
+                const uint32_t e = orders[(size_t)r * 2 * M->n_max + t];
+                isb = e >> 15;
+                s = e & 0x7FFFu;
+                if ((isb ? bi : fi) >= n) return false;
+                (isb ? bi : fi)++;
+            } else {
+                isb = (fb[(t / 32) * P + r] >> (t % 32)) & 1u;
+                if ((isb ? bi : fi) >= n) return false;
+                s = isb ? bwd[bi++] : fwd[fi++];
+            }
             if (s >= M->n_max || !present[s]) return false;
-            (isb ? S.slotB : S.slotF)[r * M->n_max + s] = t;
+            uint32_t &slot = (isb ? S.slotB : S.slotF)[r * M->n_max + s];
+            if (slot != ~0u) return false;                       // the same segment twice on this rank
+            slot = t;
             S.seg[r * 2 * n + t] = s;
             S.dir[r * 2 * n + t] = (uint8_t)isb;
             uint32_t q = 0;
@@ -143,14 +160,14 @@ void messages(const dip_model *M, const Sched &S, const std::vector<uint8_t> &Mv
 
 }  // namespace
 
-extern "C" dip_status dip_compile_plan(const dip_model *M, const void *record, const uint64_t *start,
-                                       const uint64_t *end, dip_action *actions, size_t capacity,
-                                       uint32_t *rank_off, uint32_t *n_messages) {
+extern "C" dip_status dip_compile_plan(const dip_model *M, const void *record, const uint16_t *orders,
+                                       const uint64_t *start, const uint64_t *end, dip_action *actions,
+                                       size_t capacity, uint32_t *rank_off, uint32_t *n_messages) {
     if (!M || !record || !start || !end || !rank_off) return fail(DIP_EINVAL, "null argument");
     Sched S;
     std::vector<uint8_t> Mv;
     std::vector<uint32_t> W;
-    if (!decode(M, static_cast<const uint8_t *>(record), S, Mv, W)) return fail(DIP_EINVAL, "malformed record");
+    if (!decode(M, static_cast<const uint8_t *>(record), orders, S, Mv, W)) return fail(DIP_EINVAL, "malformed record");
     const uint32_t P = S.P, n = S.n, n2 = 2 * M->n_max;   // timeline rows are 2*n_max long
     std::vector<Msg> msgs;
     messages(M, S, Mv, W, msgs);
@@ -201,8 +218,9 @@ extern "C" dip_status dip_compile_plan(const dip_model *M, const void *record, c
     return DIP_OK;
 }
 
-extern "C" dip_status dip_validate_plan(const dip_model *M, const void *record, const dip_action *actions,
-                                        const uint32_t *rank_off, uint64_t *stage_start, int32_t *ok) {
+extern "C" dip_status dip_validate_plan(const dip_model *M, const void *record, const uint16_t *orders,
+                                        const dip_action *actions, const uint32_t *rank_off, uint64_t *stage_start,
+                                        int32_t *ok) {
     // discrete-event execution: a rank runs its list in order; isend / irecv post instantly; a
     // wait_irecv completes when the message has arrived (send time + p2p); a wait_isend when the
     // receive has been posted; a stage starts at the rank's clock and runs for its latency.
@@ -211,11 +229,23 @@ extern "C" dip_status dip_validate_plan(const dip_model *M, const void *record, 
     Sched S;
     std::vector<uint8_t> Mv;
     std::vector<uint32_t> W;
-    if (!decode(M, static_cast<const uint8_t *>(record), S, Mv, W)) return fail(DIP_EINVAL, "malformed record");
+    if (!decode(M, static_cast<const uint8_t *>(record), orders, S, Mv, W)) return fail(DIP_EINVAL, "malformed record");
     const uint32_t P = S.P, n = S.n, n2 = 2 * M->n_max;
     std::vector<Msg> msgs;
     messages(M, S, Mv, W, msgs);
     const size_t nmsg = msgs.size();
+    for (uint32_t r = 1; r <= P; r++)
+        if (rank_off[r] < rank_off[r - 1]) return fail(DIP_EINVAL, "rank_off not monotone");
+    for (uint32_t r = 0; r < P; r++)          // caller-supplied actions: reject out-of-range fields
+        for (uint32_t a = rank_off[r]; a < rank_off[r + 1]; a++) {
+            const dip_action &x = actions[a];
+            if (x.kind > DIP_ACT_WAIT_IRECV) return DIP_OK;
+            if ((x.kind == DIP_ACT_FW_STAGE || x.kind == DIP_ACT_BW_STAGE) &&
+                (x.slot >= 2 * n || S.dir[r * 2 * n + x.slot] != (x.kind == DIP_ACT_BW_STAGE ? 1u : 0u)))
+                return DIP_OK;
+            if (x.kind >= DIP_ACT_ISEND && x.tag >= nmsg) return DIP_OK;
+        }
+
     std::vector<int64_t> sent(nmsg, -1), posted(nmsg, -1);
     std::vector<uint32_t> nsend(nmsg, 0), nrecv(nmsg, 0);
     std::vector<uint32_t> pc(P);

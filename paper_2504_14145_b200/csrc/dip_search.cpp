@@ -154,8 +154,8 @@ void build_record(const dip_model *Md, const Setup &S, const std::vector<uint32_
 }  // namespace
 
 extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const uint8_t *split,
-                                 const dip_search_params *prm, void *best_record_out, double *trace,
-                                 dip_search_result *out, void *stream) {
+                                 const dip_search_params *prm, void *best_record_out, uint16_t *best_orders_out,
+                                 double *trace, dip_search_result *out, void *stream) {
     if (!Md || !w || w->model != Md || !split || !prm || !out) return fail(DIP_EINVAL, "null argument");
     if (prm->rounds == 0 || prm->leaves == 0 || prm->rollouts == 0) return fail(DIP_EINVAL, "empty budget");
     if (prm->memopt && !Md->S) return fail(DIP_EINVAL, "memopt rollouts need a strategy menu (dip_set_strategies)");
@@ -205,10 +205,14 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     uint8_t *d_rec = nullptr;
     dip_result *d_res = nullptr;
     uint8_t *d_sel = nullptr;
+    uint16_t *d_ord = nullptr;
+    const size_t ord_elems = (size_t)Md->P * 2 * Md->n_max;     // per-rank orders of one rollout
     CUDA_TRY(cudaMalloc(&d_rec, cap * Md->stride));
     if (cudaMalloc(&d_res, cap * sizeof(dip_result)) != cudaSuccess) { cudaFree(d_rec); return fail(DIP_ENOMEM, "search buffers"); }
-    if (prm->memopt && cudaMalloc(&d_sel, cap * Md->P * 2ull * Md->n_max) != cudaSuccess) {
+    if (cudaMalloc(&d_ord, cap * ord_elems * 2) != cudaSuccess ||
+        (prm->memopt && cudaMalloc(&d_sel, cap * Md->P * 2ull * Md->n_max) != cudaSuccess)) {
         cudaFree(d_rec); cudaFree(d_res);
+        if (d_ord) cudaFree(d_ord);
         return fail(DIP_ENOMEM, "search buffers");
     }
     std::vector<Node> tree(1);
@@ -319,10 +323,10 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
             status = fail(DIP_ECUDA, "search H2D");
             break;
         }
-        status = dip_interleave(Md, w, d_rec, cnt, d_res, nullptr, stream);
+        status = dip_interleave(Md, w, d_rec, cnt, d_res, nullptr, d_ord, stream);
         if (status != DIP_OK) break;
         if (prm->memopt) {   // interleaving, then per-layer memory optimisation (f3)
-            status = dip_memopt(Md, w, d_rec, cnt, d_sel, d_res, nullptr, stream);
+            status = dip_memopt(Md, w, d_rec, d_ord, cnt, d_sel, d_res, nullptr, stream);
             if (status != DIP_OK) break;
         }
         if (cudaMemcpyAsync(h_res.data(), d_res, cnt * sizeof(dip_result), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -353,6 +357,12 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
                 break;
             }
         }
+        if (arg < cnt && best_orders_out) {
+            if (cudaMemcpy(best_orders_out, d_ord + arg * ord_elems, ord_elems * 2, cudaMemcpyDeviceToHost) != cudaSuccess) {
+                status = fail(DIP_ECUDA, "search best orders");
+                break;
+            }
+        }
         if (trace) trace[rd] = best;
         t_back += now() - t3;
     }
@@ -361,6 +371,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
                      t_sel * 1e3, t_build * 1e3, t_gpu * 1e3, t_back * 1e3, rd);
     cudaFree(d_rec);
     cudaFree(d_res);
+    cudaFree(d_ord);
     if (d_sel) cudaFree(d_sel);
     if (status != DIP_OK) return status;
     out->found = best > 0.0;

@@ -103,8 +103,9 @@ def lib():
     L.dip_workspace_create.argtypes = [vp, ctypes.c_size_t, ctypes.POINTER(vp)]
     L.dip_workspace_free.argtypes = [vp]
     L.dip_eval_schedules.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
-    L.dip_interleave.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp]
-    L.dip_search.argtypes = [vp, vp, vp, ctypes.POINTER(_SearchParams), vp, vp, ctypes.POINTER(_SearchResult), vp]
+    L.dip_interleave.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    L.dip_eval_orders.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp, vp, vp]
+    L.dip_search.argtypes = [vp, vp, vp, ctypes.POINTER(_SearchParams), vp, vp, vp, ctypes.POINTER(_SearchResult), vp]
     L.dip_argmin.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp,
                              ctypes.POINTER(_Winner), vp]
     L.dip_eval_host.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
@@ -113,19 +114,20 @@ def lib():
                                ctypes.POINTER(ctypes.c_uint64)]
     L.dip_unpack_key.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_Winner)]
     L.dip_timeline.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
-    L.dip_compile_plan.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(ctypes.c_uint32)]
-    L.dip_validate_plan.argtypes = [vp, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_int32)]
+    L.dip_compile_plan.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, ctypes.POINTER(ctypes.c_uint32)]
+    L.dip_validate_plan.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_int32)]
     L.dip_set_strategies.argtypes = [vp, ctypes.c_uint32, vp, vp, vp, ctypes.c_uint32]
     L.dip_strategy_candidates.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp,
                                           ctypes.POINTER(ctypes.c_uint32)]
-    L.dip_memopt.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    L.dip_memopt.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
     L.dip_set_memopt_solver.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32]
     L.dip_memopt_stats.argtypes = [vp, vp, vp]
     L.dip_comm_unique_id.argtypes = [vp]
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
     for f in ("dip_load_cost_model", "dip_model_free", "dip_model_get_info", "dip_encode_candidates",
-              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_interleave", "dip_search",
+              "dip_workspace_create", "dip_workspace_free", "dip_eval_schedules", "dip_interleave", "dip_eval_orders",
+              "dip_search",
               "dip_argmin",
               "dip_eval_host",
               "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key",
@@ -305,18 +307,31 @@ def eval_schedules(model: Model, ws: Workspace, d_records, count: int, d_results
                                     _ptr(d_peaks), _stream(stream)), "dip_eval_schedules")
 
 
-def interleave(model: Model, ws: Workspace, d_records, count: int, d_results, d_peaks=None, stream=None):
-    """f1: build each record's F/B interleaving in place with DIP's dual-queue greedy
-    and score it (results as eval_schedules)."""
+def interleave(model: Model, ws: Workspace, d_records, count: int, d_results, d_peaks=None, d_orders=None,
+               stream=None):
+    """f1: DIP's dual-queue greedy on each record's split and priority orders; scores
+    the built schedule (results as eval_schedules) and, with d_orders ([count][P][2 n_max] u16
+    device), emits every rank's stage order (segment id | 0x8000 for backward, 0xFFFF padding)."""
     _check(lib().dip_interleave(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_results),
-                                _ptr(d_peaks), _stream(stream)), "dip_interleave")
+                                _ptr(d_peaks), _ptr(d_orders), _stream(stream)), "dip_interleave")
 
 
-def memopt(model: Model, ws: Workspace, d_records, count: int, d_sel, d_results, d_peaks=None, stream=None):
+def eval_orders(model: Model, ws: Workspace, d_records, d_orders, count: int, d_results, d_peaks=None, d_sel=None,
+                d_start=None, d_end=None, stream=None):
+    """Score schedules given as explicit per-rank orders (interleave's output format), optionally
+    with an f3 selection (d_sel) and per-slot timelines (d_start / d_end [count][P][2 n_max] u64)."""
+    _check(lib().dip_eval_orders(model.handle, ws.handle, _ptr(d_records), _ptr(d_orders), count, _ptr(d_sel),
+                                 _ptr(d_results), _ptr(d_peaks), _ptr(d_start), _ptr(d_end), _stream(stream)),
+           "dip_eval_orders")
+
+
+def memopt(model: Model, ws: Workspace, d_records, count: int, d_sel, d_results, d_peaks=None, stream=None,
+           d_orders=None):
     """f3: per-rank strategy selection (d_sel [count][P][2][n_max] u8 out) and the
-    re-timed scores (results as eval_schedules)."""
-    _check(lib().dip_memopt(model.handle, ws.handle, _ptr(d_records), count, _ptr(d_sel), _ptr(d_results),
-                            _ptr(d_peaks), _stream(stream)), "dip_memopt")
+    re-timed scores (results as eval_schedules); with d_orders the ranks' orders are those explicit
+    per-rank orders (interleave's output) instead of the records' sequences + F/B bits."""
+    _check(lib().dip_memopt(model.handle, ws.handle, _ptr(d_records), _ptr(d_orders), count, _ptr(d_sel),
+                            _ptr(d_results), _ptr(d_peaks), _stream(stream)), "dip_memopt")
 
 
 def set_memopt_solver(model: Model, gap_permille: int = 50, node_cap: int = 4096):
@@ -335,16 +350,18 @@ def memopt_stats(ws: Workspace, stream=None) -> dict:
 def search(model: Model, ws: Workspace, split, seed: int, rounds: int, leaves: int, rollouts: int,
            alpha: float = 1.0, beta: float = 0.5, threads: int = 0, stream=None, memopt: bool = False) -> dict:
     """f2: MCTS over class orders for a fixed split with batched GPU rollouts.
-    Returns dict(found, makespan, score, trace, record (host bytes of the best schedule), ...)."""
+    Returns dict(found, makespan, score, trace, record (host bytes of the best rollout's split and
+    priority orders), orders ([P, 2 n_max] its per-rank orders), ...)."""
     sp = np.ascontiguousarray(np.asarray(split, np.uint8).reshape(-1))
     prm = _SearchParams(seed & ((1 << 64) - 1), rounds, leaves, rollouts, threads, alpha, beta, 1 if memopt else 0)
     out = _SearchResult()
     rec = np.zeros(model.stride, np.uint8)
+    ords = np.zeros((model.P, 2 * model.n_max), np.uint16)
     trace = np.zeros(rounds, np.float64)
     _check(lib().dip_search(model.handle, ws.handle, sp.ctypes.data, ctypes.byref(prm), rec.ctypes.data,
-                            trace.ctypes.data, ctypes.byref(out), _stream(stream)), "dip_search")
+                            ords.ctypes.data, trace.ctypes.data, ctypes.byref(out), _stream(stream)), "dip_search")
     return dict(found=bool(out.found), makespan=out.makespan_ns, score=out.score, trace=trace, record=rec,
-                rounds_done=out.rounds_done, scored=out.rollouts_scored, tree_nodes=out.tree_nodes)
+                orders=ords, rounds_done=out.rounds_done, scored=out.rollouts_scored, tree_nodes=out.tree_nodes)
 
 
 def timeline(model: Model, ws: Workspace, d_records, count: int, d_results, d_start, d_end, stream=None):
@@ -353,10 +370,12 @@ def timeline(model: Model, ws: Workspace, d_records, count: int, d_results, d_st
                               _ptr(d_end), _stream(stream)), "dip_timeline")
 
 
-def compile_plan(model: Model, record, start, end):
+def compile_plan(model: Model, record, start, end, orders=None):
     """f4 (P:717-734): per-rank action lists of one schedule. record: host uint8[stride];
-    start / end: host uint64 [P, 2*n_max]. Returns (actions structured array, rank_off, n_messages)."""
+    start / end: host uint64 [P, 2*n_max]; orders: None (the record's sequences + bits) or host
+    [P, 2*n_max] u16 per-rank orders (interleave's output). Returns (actions, rank_off, n_messages)."""
     rec = np.ascontiguousarray(record, np.uint8)
+    od = None if orders is None else np.ascontiguousarray(orders, np.uint16)
     st = np.ascontiguousarray(start, np.uint64)
     en = np.ascontiguousarray(end, np.uint64)
     off = np.zeros(model.P + 1, np.uint32)
@@ -364,8 +383,9 @@ def compile_plan(model: Model, record, start, end):
     cap = 1 << 16
     while True:
         acts = np.zeros((cap, 5), np.uint32)
-        code = lib().dip_compile_plan(model.handle, rec.ctypes.data, st.ctypes.data, en.ctypes.data,
-                                      acts.ctypes.data, cap, off.ctypes.data, ctypes.byref(nmsg))
+        code = lib().dip_compile_plan(model.handle, rec.ctypes.data, None if od is None else od.ctypes.data,
+                                      st.ctypes.data, en.ctypes.data, acts.ctypes.data, cap, off.ctypes.data,
+                                      ctypes.byref(nmsg))
         if code == 4 and off[-1] > cap:   # DIP_ERANGE: grow
             cap = int(off[-1])
             continue
@@ -373,15 +393,17 @@ def compile_plan(model: Model, record, start, end):
         return acts[: off[-1]], off, nmsg.value
 
 
-def validate_plan(model: Model, record, acts, off):
+def validate_plan(model: Model, record, acts, off, orders=None):
     """Discrete-event execution of a plan -> (ok, stage start times [P, 2*n_max])."""
     rec = np.ascontiguousarray(record, np.uint8)
+    od = None if orders is None else np.ascontiguousarray(orders, np.uint16)
     a = np.ascontiguousarray(acts, np.uint32)
     o = np.ascontiguousarray(off, np.uint32)
     st = np.zeros((model.P, 2 * model.n_max), np.uint64)
     ok = ctypes.c_int32()
-    _check(lib().dip_validate_plan(model.handle, rec.ctypes.data, a.ctypes.data, o.ctypes.data, st.ctypes.data,
-                                   ctypes.byref(ok)), "dip_validate_plan")
+    _check(lib().dip_validate_plan(model.handle, rec.ctypes.data, None if od is None else od.ctypes.data,
+                                   a.ctypes.data, o.ctypes.data, st.ctypes.data, ctypes.byref(ok)),
+           "dip_validate_plan")
     return bool(ok.value), st
 
 

@@ -175,3 +175,38 @@ def test_strategy_menu_guards():
     assert e.value.code == 4
     m.set_strategies((f, b, a), 10)                    # and a valid menu still loads afterwards
     assert m.strategy_candidates(1, oracle.chunk_layers(pb.modules[1].L, pb.P, pb.modules[1].K)[0], 5)
+
+
+@pytest.mark.parametrize("name,count", [("toy", 128), ("12B", 128), ("T2V", 32), ("94B", 16)])
+def test_memopt_on_interleaved_orders(name, count):
+    """f2's rollout: dip_interleave's per-rank orders -> dip_memopt on those orders ->
+    re-timing with the selection (dip_eval_orders); selections, scores and peaks == the oracle's
+    M1-M4 on the oracle's own interleaving"""
+    pb = gen.make_problem(name)
+    menu = strategy_menu(pb)
+    cs = gen.generate(pb, 0, count, mode=1 if name == "toy" else 0, p_mutate=0.0, p_bad=0.02)
+    m = dip.Model(pb, 0)
+    m.set_strategies(menu, 10)
+    ws = dip.Workspace(m)
+    s = torch.cuda.current_stream()
+    d_rec = torch.from_numpy(m.encode(cs)).cuda()
+    d_res = torch.empty(count * 24, dtype=torch.uint8, device="cuda")
+    d_pk = torch.empty((count, pb.P), dtype=torch.int32, device="cuda")
+    d_ord = torch.empty((count, pb.P, 2 * pb.n_max), dtype=torch.int16, device="cuda")
+    d_sel = torch.empty(count * pb.P * 2 * pb.n_max, dtype=torch.uint8, device="cuda")
+    dip.interleave(m, ws, d_rec, count, d_res, None, d_orders=d_ord, stream=s)
+    dip.memopt(m, ws, d_rec, count, d_sel, d_res, d_pk, stream=s, d_orders=d_ord)
+    torch.cuda.synchronize()
+    res = dip.results_view(d_res.cpu().numpy()).copy()
+    sel = d_sel.cpu().numpy().reshape(count, pb.P, 2, pb.n_max)
+    rords, _ = oracle.interleave(pb, cs, threads=16)
+    assert np.array_equal(d_ord.cpu().numpy().view(np.uint16), rords)
+    rsel, ref = oracle.memopt(pb, cs, menu, S=10, threads=16, orders=rords)
+    assert np.array_equal(res["status"], ref.status)
+    good = ref.status != oracle.ST_BAD
+    assert np.array_equal(sel[good], rsel[good])
+    assert np.array_equal(res["makespan_ns"], ref.makespan)
+    assert np.array_equal(res["bubble"].view(np.uint64), ref.bubble.view(np.uint64))
+    assert np.array_equal(d_pk.cpu().numpy().view(np.uint32).astype(np.uint64), ref.peaks)
+    if name != "toy":
+        assert sel[good].any()

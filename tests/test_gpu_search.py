@@ -13,7 +13,6 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2504_14145_b200 as dip  # noqa: E402
-from tests.test_gpu_interleave import fb_rows  # noqa: E402
 
 
 @pytest.mark.parametrize("name,rounds,leaves,rollouts", [("toy", 30, 4, 6), ("12B", 8, 8, 8), ("T2V", 4, 4, 4),
@@ -29,10 +28,8 @@ def test_search_matches_oracle_trajectory(name, rounds, leaves, rollouts):
     o = oracle.search(pb, split, seed=9, rounds=rounds, leaves=leaves, rollouts=rollouts, alpha=1.0, beta=0.5)
     assert np.array_equal(g["trace"], o["trace"])
     assert g["makespan"] == o["makespan"] and g["score"] == o["score"]
-    rec = g["record"]
-    n = int(cs.n[0])
-    assert np.array_equal(fb_rows(pb, m, rec[None, :])[0], o["bits"])
-    assert g["scored"] == rounds * leaves * rollouts or g["scored"] <= rounds * leaves * rollouts
+    assert np.array_equal(g["orders"], o["orders"])
+    assert g["scored"] == o["scored"]
 
 
 @pytest.mark.parametrize("name,rounds,leaves,rollouts", [("toy", 12, 4, 4), ("12B", 6, 8, 6), ("T2V", 3, 4, 3)])
@@ -52,4 +49,21 @@ def test_search_with_memopt_matches_oracle_trajectory(name, rounds, leaves, roll
                       menu=menu, S=10)
     assert np.array_equal(g["trace"], o["trace"])
     assert g["makespan"] == o["makespan"] and g["score"] == o["score"]
-    assert np.array_equal(fb_rows(pb, m, g["record"][None, :])[0], o["bits"])
+    assert np.array_equal(g["orders"], o["orders"])
+
+
+def test_search_beats_templates_on_94B_winner_split():
+    """on the split of the 94B bench winner, the GPU search (8 rounds x 64 leaves x
+    4 rollouts) reaches a makespan no worse than the generator's own template orders run through f1,
+    and far below the same orders at fixed order"""
+    pb = gen.make_problem("94B")
+    cs = gen.generate(pb, 2696, 1)
+    fixed = oracle.evaluate(pb, cs)
+    _, tf1 = oracle.interleave(pb, cs)
+    m = dip.Model(pb, 0)
+    ws = dip.Workspace(m)
+    g = dip.search(m, ws, cs.split[0], seed=pb.seed, rounds=8, leaves=64, rollouts=4, alpha=1.0, beta=0.5,
+                   stream=torch.cuda.current_stream())
+    assert g["found"] and g["makespan"] <= int(tf1.makespan[0]) < int(fixed.makespan[0])
+    print(f"RESULT f2 94B winner split: search {g['makespan']} ns, template f1 {int(tf1.makespan[0])} ns, "
+          f"template fixed order {int(fixed.makespan[0])} ns")

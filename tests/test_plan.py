@@ -136,3 +136,53 @@ def test_broken_plans_are_rejected(dip):
     # and make rank 0 wait for rank 1's backward first: a cycle through the waits
     dead = np.concatenate([moved, acts[off[1]:]])
     assert not dip.validate_plan(m, rec, dead, off)[0]
+
+
+def test_malformed_records_and_orders_are_rejected(dip):
+    """a record whose forward sequence repeats a segment, or per-rank orders with a duplicated /
+    missing stage, is DIP_EINVAL for compile and validate -- not a crash (an id that never gets a
+    slot used to index the post lists out of range)"""
+    from paper_2504_14145_b200.dip import DipError
+    pb = H.uniform_problem(4, 4, 1, 2, K=2, p2p=1)
+    cs = H.candidates_from_orders(pb, [[1] * 4], [H.vpp(4, 2, 4)])
+    m = dip.Model(pb, -1)
+    st, S, E = oracle_rows(pb, cs, 0)
+    good = m.encode(cs)
+    acts, off, nmsg = dip.compile_plan(m, good, S, E)
+    bad = cs.subset([0])
+    bad.fwd[0, 1] = bad.fwd[0, 0]
+    with pytest.raises(DipError) as e:
+        dip.compile_plan(m, m.encode(bad), S, E)
+    assert e.value.code == 1
+    with pytest.raises(DipError):
+        dip.validate_plan(m, m.encode(bad), acts, off)
+    ords = H.orders_array(pb, H.vpp(4, 2, 4))
+    acts2, off2, _ = dip.compile_plan(m, good, S, E, orders=ords)      # the same schedule as orders
+    assert np.array_equal(acts2, acts) and np.array_equal(off2, off)
+    for mut in ("dup", "missing"):
+        o2 = ords.copy()
+        if mut == "dup":
+            o2[2, 3] = o2[2, 2] if (o2[2, 2] & 0x8000) == (o2[2, 3] & 0x8000) else o2[2, 1]
+        else:
+            o2[1, 0] = 0xFFFF
+        with pytest.raises(DipError):
+            dip.compile_plan(m, good, S, E, orders=o2)
+
+
+def test_validator_rejects_out_of_range_actions(dip):
+    """caller-supplied plans: a stage slot beyond 2n, a stage of the wrong direction, or a wait on an
+    unknown tag make the plan invalid (ok = 0) instead of indexing out of range"""
+    pb = H.uniform_problem(2, 2, 1, 2, p2p=1)
+    cs = H.candidates_from_orders(pb, [[1, 1]], [H.one_f_one_b(2, 2)])
+    m, rec, st, S, acts, off, nmsg = compile_one(dip, pb, cs, 0)
+    ok, _ = dip.validate_plan(m, rec, acts, off)
+    assert ok
+    for field, kind, value in [(4, 0, 99), (0, 0, 1), (2, 4, 1000), (2, 5, 1000)]:
+        a = acts.copy()
+        x = int(np.nonzero(a[:, 0] == kind)[0][0])
+        if field == 0:
+            a[x, 0] = value             # fw_stage -> bw_stage at a forward slot
+        else:
+            a[x, field] = value
+        ok, _ = dip.validate_plan(m, rec, a, off)
+        assert not ok, (field, kind, value)
