@@ -42,7 +42,8 @@ CONFIG_DESC = {
     "94B": "94B LMM (ViT-22B + Qwen2-72B): P=32, m=64, K_LLM=2",
 }
 INT_OPS_PER_STAGE = 10          # algorithmic int32-equivalent ops per stage node
-INT_OPS_PER_CLK_SM = 128        # 4 SMSP x 1 warp-instr/clk (ALU + FMA pipes, B300_MICROARCH.md)
+INT_OPS_PER_CLK_SM = 128        # guide figure (4 SMSP x 1 warp-instr/clk, B300_MICROARCH.md): context only;
+                                # the roofline peak is the in-repo microbenchmark (dip_ubench_int) measured live
 FALLBACK_HBM_GBS = 6650.0       # B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
@@ -212,6 +213,11 @@ def main():
     h_rec = torch.empty(per * model.stride, dtype=torch.uint8).pin_memory()
     model.encode(cs, out=h_rec, threads=gthreads)
     n_seg = cs.n.astype(np.int64)                     # per-candidate segment counts (stage-node totals)
+    # the candidates' host view in pinned memory: the input of the end-to-end measurement
+    h_view = None
+    if not args.no_e2e:
+        h_view = [torch.from_numpy(np.ascontiguousarray(getattr(cs, k))).pin_memory()
+                  for k in ("split", "n", "fwd", "bwd", "fb")]
     if world > 1:   # the host-view arrays are only needed by rank 0's single-GPU side legs: free them
         cs = cs.subset(np.arange(min(per, 64)))
     d_rec = h_rec.to(dev)
@@ -232,7 +238,11 @@ def main():
         win = step()
     res = dip.results_view(d_res.cpu().numpy())
     hist = np.bincount(res["status"], minlength=4).tolist()
-    stages = int(np.sum(np.where(res["status"] != 3, 2 * n_seg * pb.P, 0)))
+    # algorithmic work: the stage nodes of fully timed candidates (OK and OOM); a DEADLOCK candidate's
+    # partial wavefront and a BAD_ENCODING record count nothing
+    timed = (res["status"] == 0) | (res["status"] == 1)
+    stages = int(np.sum(np.where(timed, 2 * n_seg * pb.P, 0)))
+    ub = dip.ubench_int(local) if rank == 0 else None     # the integer-pipe peak, measured on this GPU
 
     # ---- timed region: device-resident inputs
     if world > 1:
@@ -259,31 +269,56 @@ def main():
     if world > 1:
         dist.barrier()
     t_ms = sum(a.elapsed_time(b) for a, b in zip(s0, s1))
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(s0, k1))
-    tt = torch.tensor([t_ms, kern_ms], dtype=torch.float64, device=dev)
+    kts = [a.elapsed_time(b) for a, b in zip(s0, k1)]
+    sts = [a.elapsed_time(b) for a, b in zip(s0, s1)]
+    kern_ms = statistics.mean(kts)
+    tt = torch.tensor([t_ms, kern_ms, statistics.median(kts), min(kts), statistics.median(sts), min(sts)],
+                      dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms, kern_ms = float(tt[0]), float(tt[1])
+    step_stats = {"kernel_ms_median": float(tt[2]), "kernel_ms_min": float(tt[3]), "kernel_ms_mean": kern_ms,
+                  "step_ms_median": float(tt[4]), "step_ms_min": float(tt[5]), "step_ms_mean": t_ms / args.steps,
+                  "value_at_median_step": per * world / (float(tt[4]) / 1e3),
+                  "value_at_min_step": per * world / (float(tt[5]) / 1e3)}
     value = per * world * args.steps / (t_ms / 1e3)
 
-    # ---- end to end through the public host API: pinned host records -> H2D -> score -> winner D2H
+    # ---- end to end through the public host API, from the candidates' HOST VIEW (pinned split, n,
+    # fwd, bwd, fb arrays): chunked H2D -> device encode (the word-major transpose on the GPU) ->
+    # scoring -> every result D2H (24 B per candidate) -> winner
     e2e = None
     if not args.no_e2e:
+        h_res = torch.empty(per * 24, dtype=torch.uint8).pin_memory()
         for _ in range(2):
-            dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+            dip.eval_host_view(model, ws, h_view, per, h_res, per, rank, world, comm, stream=stream)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
-            w2 = dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+            w2 = dip.eval_host_view(model, ws, h_view, per, h_res, per, rank, world, comm, stream=stream)
         b.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         assert w2.global_index == win.global_index and w2.makespan_ns == win.makespan_ns
+        hres = dip.results_view(h_res.numpy())
+        assert np.array_equal(hres["makespan_ns"], res["makespan_ns"]) and np.array_equal(hres["status"], res["status"])
+        view_bytes = sum(t.numel() * t.element_size() for t in h_view)
+        # the older record path (pinned records, no encode inside the timed region), for comparison
+        for _ in range(2):
+            dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.steps):
+            dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tr = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
         # the copy alone: what bounds the end-to-end number when it is below the device number
         a.record(stream)
         d_rec.copy_(h_rec, non_blocking=True)
@@ -291,12 +326,16 @@ def main():
         torch.cuda.synchronize()
         h2d = per * model.stride / (a.elapsed_time(b) / 1e3) / 1e9
         e2e = {"value": per * world * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": per * model.stride, "d2h_bytes_per_step": 8,
+               "h2d_bytes_per_step": view_bytes, "d2h_bytes_per_step": per * 24 + 8,
                "h2d_GBps_alone": h2d,
-               "path": "dip_eval_host: pinned host records, 64K-record chunks, H2D overlapped with scoring"}
+               "path": "dip_eval_host_view: the candidates' host-view arrays (pinned) -> chunked H2D -> "
+                       "dip_encode_candidates_device -> dip_eval_schedules -> all results D2H -> dip_argmin",
+               "records_path": {"value": per * world * args.steps / (float(tr[0]) / 1e3), "unit": UNIT,
+                                "path": "dip_eval_host: pre-encoded pinned records -> H2D -> score -> winner"}}
 
     # ---- DIP's dual-queue interleaving on the first f1-count records
     f1 = None
+    f1_first = None
     try:
         if args.f1_count > 0:
             cnt = min(per, args.f1_count)
@@ -316,6 +355,7 @@ def main():
             tf1 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(tf1, op=dist.ReduceOp.MAX)
+            f1_first = dip.results_view(r_f1[:24].cpu().numpy())[0]     # candidate 0 through f1 (for f2)
             f1 = {"what": "dip_interleave: build each candidate's per-rank stage orders with the paper's dual-queue "
                           "greedy (P:511-548, priority queues over ready stages) from its split + priority orders, "
                           "emit the orders and score them",
@@ -359,10 +399,12 @@ def main():
             base = dip.results_view(d_res[: cnt * 24].cpu().numpy())
             ok = (r3["status"] == 0) & (base["status"] == 0)
             gain = float(np.median(r3["makespan_ns"][ok] / base["makespan_ns"][ok])) if ok.any() else None
-            f3 = {"what": "dip_memopt: per-rank greedy strategy selection under the memory budget (P:569-590) "
-                          "over GPU-built knapsack candidates (P:558-567, S = 10, 3 strategies), then re-timing",
+            f3 = {"what": "dip_memopt: per-rank ILP (P:569-590) solved to a 5% gap -- greedy warm start, Lagrangian "
+                          "bound, branch and bound -- over GPU-built knapsack candidates (P:558-567, S = 10, 3 "
+                          "strategies), then re-timing",
                   "value": cnt * world * reps / (float(tf3[0]) / 1e3), "unit": "candidates/s",
                   "candidates_per_gpu": cnt, "ms_per_call": float(tf3[0]) / reps,
+                  "solver": dip.memopt_stats(ws, stream=stream),
                   "median_makespan_ratio_vs_base": gain}
             if rank == 0 and world == 1 and not args.no_cpu_baseline:
                 import oracle
@@ -390,7 +432,9 @@ def main():
                           "-> score, one batched GPU launch per round",
                   "rollouts_per_s": sr["scored"] / dt, "rollouts": sr["scored"], "rounds": sr["rounds_done"],
                   "wall_s": dt, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
-                  "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"]}
+                  "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"],
+                  "same_split_template_fixed_order_ns": int(res["makespan_ns"][0]),
+                  "same_split_template_f1_ns": int(f1_first["makespan_ns"]) if f1_first is not None else None}
             if world == 1 and not args.no_cpu_baseline:   # the oracle's search (single-threaded), 1 round x 64 leaves
                 import oracle
                 t0 = time.perf_counter()
@@ -409,7 +453,10 @@ def main():
         clocks = clk.summary()
         kern_s = kern_ms / 1e3
         ops = INT_OPS_PER_STAGE * stages
-        alu_peak = INT_OPS_PER_CLK_SM * 148 * sm_max * 1e6
+        # measured integer-instruction peak: the fastest sustained integer kind of the microbenchmark
+        alu_kinds = ("IADD3", "VIMNMX", "ISETP+SEL", "IADD3+IADD3.X (u64 add)", "IMAD")
+        alu_peak = max(ub[k] for k in alu_kinds)
+        alu_peak_kind = max(alu_kinds, key=lambda k: ub[k])
         bytes_launch = per * (model.stride + 24 + 4 * pb.P)
         traffic = None
         tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
@@ -438,8 +485,13 @@ def main():
                          "traffic_source": "profiles/ncu_traffic_%s.json (per-candidate DRAM bytes x candidates per launch)" % args.config,
                          "algorithmic_bytes": bytes_launch,
                          "kernel": "dip_eval_kernel", "kernel_ms": kern_ms,
-                         "algorithmic": f"{INT_OPS_PER_STAGE} int32 ops x {stages} stage nodes per launch",
-                         "peak_source": f"128 int32 ops/clk/SM x 148 SMs x {sm_max:.0f} MHz ({src} sm_max)"},
+                         "algorithmic": f"{INT_OPS_PER_STAGE} int32 ops x {stages} stage nodes of the launch's "
+                                        f"timed (OK / OOM) candidates",
+                         "peak_source": f"measured: dip_ubench_int, {alu_peak_kind} (the fastest integer kind), "
+                                        f"thread instructions/s over all 148 SMs at the run's clocks",
+                         "ubench_Tinst_per_s": {k: v / 1e12 for k, v in ub.items()},
+                         "guide_peak": INT_OPS_PER_CLK_SM * 148 * sm_max * 1e6 / 1e12},
+            "timing": step_stats,
             "hbm": {"achieved": bytes_launch / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bytes_launch / kern_s / 1e9 / hbm_peak,
                     "algorithmic": "record + 24 B result + 4P B peaks per candidate", "peak_source": src},

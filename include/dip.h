@@ -131,6 +131,13 @@ typedef struct {
 dip_status dip_encode_candidates(const dip_model *m, const dip_candidate_batch *c, size_t count,
                                  void *out_records, int threads);
 
+/* SURVEY §8(b)'s device mode of dip_encode_candidates: the batch's five arrays are DEVICE pointers
+ * (same layouts as above); the records are written to device memory d_out (count * record_stride
+ * bytes) by a GPU kernel (the F/B rows' rank-major -> word-major transpose runs on the GPU),
+ * byte-identical to the host encoder. Asynchronous on `stream`. */
+dip_status dip_encode_candidates_device(const dip_model *m, const dip_candidate_batch *d_batch, size_t count,
+                                        void *d_out, void *stream);
+
 /* 24-byte result per candidate. BAD_ENCODING/DEADLOCK: makespan = UINT64_MAX,
  * bubble = -1.0. bubble = (P*makespan - sum of busy ns) / (P*makespan) as one IEEE
  * double division of exact integers (R-16); 0.0 when P*makespan = 0. */
@@ -307,6 +314,15 @@ dip_status dip_unpack_key(uint64_t key, uint64_t shard_stride, uint32_t world, d
 /* End to end from HOST records (pinned for overlap): chunked H2D copies overlapped
  * with scoring (chunks of min(host_chunk, max(8192, count/8)) records), then dip_argmin. h_results ([count], host) may be NULL. Requires a
  * workspace created with host_chunk > 0. Synchronous. */
+/* End to end from the candidates' HOST VIEW (the dip_candidate_batch arrays in host memory; pinned
+ * for full copy speed): per chunk of the workspace's host_chunk, H2D of the chunk's arrays, the
+ * device encoder (dip_encode_candidates_device), dip_eval_schedules, the D2H of its results (if
+ * h_results != NULL), copies overlapped with encode + scoring; then dip_argmin as dip_eval_host.
+ * Synchronous. The device staging for the host view is allocated on first use. */
+dip_status dip_eval_host_view(const dip_model *m, dip_workspace *w, const dip_candidate_batch *h_batch, size_t count,
+                              dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world,
+                              dip_comm *comm, dip_winner *out, void *stream);
+
 dip_status dip_eval_host(const dip_model *m, dip_workspace *w, const void *h_records, size_t count,
                          dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world,
                          dip_comm *comm, dip_winner *out, void *stream);
@@ -339,6 +355,13 @@ dip_status dip_compile_plan(const dip_model *m, const void *record, const uint16
  * NULL) receives each stage's start time, which equals the source timeline for compiled plans. */
 dip_status dip_validate_plan(const dip_model *m, const void *record, const uint16_t *orders, const dip_action *actions,
                              const uint32_t *rank_off, uint64_t *stage_start, int32_t *ok);
+
+/* Integer-pipe microbenchmark (the scorer's ALU roofline denominator, measured on this device):
+ * kind 0 IADD3, 1 VIMNMX (min / max), 2 ISETP + SEL, 3 SHFL.BFLY + add, 4 64-bit add (IADD3 +
+ * IADD3.X), 5 IMAD; *ops_per_s = thread-level SASS instructions per second over the whole GPU
+ * (8 independent chains per thread, every SM full), *ms = the best of 5 launches (or NULL).
+ * Synchronous. */
+dip_status dip_ubench_int(uint32_t kind, int cuda_device, double *ops_per_s, double *ms);
 
 /* NCCL communicator for the argmin: rank 0 calls dip_comm_unique_id, broadcasts
  * the 128 bytes (e.g. over torch.distributed), every rank calls dip_comm_init. */

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libdip.so")
 SRCS = [os.path.join(HERE, "csrc", f) for f in ("dip_kernels.cu", "dip_order.cu", "dip_host.cpp", "dip_search.cpp",
-                                                  "dip_plan.cpp", "dip_memopt.cu", "dip_memopt_host.cpp")]
+                                                  "dip_plan.cpp", "dip_memopt.cu", "dip_memopt_host.cpp", "dip_ubench.cu", "dip_encode.cu")]
 DEPS = SRCS + [os.path.join(HERE, "csrc", h) for h in ("dip_internal.h", "dip_host_internal.h")] + \
     [os.path.join(ROOT, "include", "dip.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

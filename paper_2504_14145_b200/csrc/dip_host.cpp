@@ -272,6 +272,7 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
         kp.o_sl = oput(2 * 8 * n_max);
         kp.o_h = oput(2 * n_max);
         kp.o_bm = oput(2 * 4 * P * nwd);
+        kp.o_sum = oput(2 * 4 * P);
         kp.o_mb = oput(3 * m * nm);
         kp.o_bytes = oo;
     }
@@ -304,7 +305,7 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     M->smem = best_smem;
     M->grid = M->num_sms * best_bps;
     CUDA_TRY(dipk::prepare_eval(G, best_smem));
-    {   // the per-rank-order kernel's shape
+    if (n_max <= 1024) {   // the per-rank-order kernel's shape (its ready-set summaries hold 32 words)
         const size_t per_warp_o = (size_t)M->cpg * kp.o_bytes;
         int bw = 0, bwpb = 0, bbps = 0;
         size_t bsm = 0;
@@ -458,11 +459,18 @@ dip_status dip_workspace_free(dip_workspace *w) {
     if (w->ev_start) cudaEventDestroy(w->ev_start);
     if (w->ev_join) cudaEventDestroy(w->ev_join);
     if (w->d_spill2) cudaFree(w->d_spill2);
+    for (int b = 0; b < dip_workspace::NBUF; b++)
+        if (w->d_view[b]) cudaFree(w->d_view[b]);
     delete w;
     return DIP_OK;
 }
 
 // ---------------------------------------------------------------- eval -----------------
+static const bool g_scorer_segment = std::getenv("DIP_SCORER") && std::string(std::getenv("DIP_SCORER")) == "segment";
+static dip_status launch_orders(const dip_model *M, dip_workspace *w, const void *d_records, size_t count, int om,
+                                const uint16_t *orders_in, uint16_t *orders_out, const uint8_t *sel,
+                                dip_result *d_results, uint32_t *d_peaks, uint64_t *d_start, uint64_t *d_end,
+                                cudaStream_t s);
 extern "C++" {
 dip_status diph::launch_chunk(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
                                uint64_t index_base, uint32_t idx_bits, bool fused, dip_result *d_results,
@@ -509,12 +517,15 @@ dip_status dip_eval_schedules(const dip_model *M, dip_workspace *w, const void *
     w->last_idx_bits = idx_bits;
     w->last_fused = fused;
     if (!count) return DIP_OK;
+    if (g_scorer_segment)   // A/B: the per-segment-state kernel on the record's own orders
+        return launch_orders(M, w, d_records, count, 2, nullptr, nullptr, nullptr, d_results, d_peaks, nullptr,
+                             nullptr, s);
     return launch_chunk(M, w, d_records, count, 0, idx_bits, fused, d_results, d_peaks, s);
 }
 
 // the per-rank-order kernel: BUILD (f1) or TIME (explicit orders, optional f3 selection / timelines)
 static dip_status launch_orders(const dip_model *M, dip_workspace *w, const void *d_records, size_t count,
-                                bool build, const uint16_t *orders_in, uint16_t *orders_out, const uint8_t *sel,
+                                int om, const uint16_t *orders_in, uint16_t *orders_out, const uint8_t *sel,
                                 dip_result *d_results, uint32_t *d_peaks, uint64_t *d_start, uint64_t *d_end,
                                 cudaStream_t s) {
     const uint32_t idx_bits = bits_for(std::max<uint64_t>(count, 2));
@@ -547,9 +558,10 @@ static dip_status launch_orders(const dip_model *M, dip_workspace *w, const void
         CUDA_TRY(cudaMemsetAsync(d_start, 0, count * M->P * 2ull * M->n_max * 8, s));
         CUDA_TRY(cudaMemsetAsync(d_end, 0, count * M->P * 2ull * M->n_max * 8, s));
     }
+    if (M->n_max > 1024) return fail(DIP_ERANGE, "per-rank-order kernel: n_max > 1024 (32 ready-set words)");
     const int grid = (int)std::min<uint64_t>((uint64_t)M->o_grid,
                                              std::max<uint64_t>(1, (count + M->cpg * M->o_wpb - 1) / (M->cpg * M->o_wpb)));
-    CUDA_TRY(dipk::launch_order(kp, M->G, build, grid, M->o_wpb * 32, M->o_smem, s));
+    CUDA_TRY(dipk::launch_order(kp, M->G, om, grid, M->o_wpb * 32, M->o_smem, s));
     g_launches++;
     return DIP_OK;
 }
@@ -559,7 +571,7 @@ dip_status dip_interleave(const dip_model *M, dip_workspace *w, const void *d_re
     if (!M || !w || w->model != M) return fail(DIP_EINVAL, "model / workspace mismatch");
     if (count && (!d_records || !d_results)) return fail(DIP_EINVAL, "null buffer");
     if (M->device < 0 || !M->d_blob) return fail(DIP_EINVAL, "host-only model (cuda_device < 0)");
-    return launch_orders(M, w, d_records, count, true, nullptr, d_orders, nullptr, d_results, d_peaks, nullptr,
+    return launch_orders(M, w, d_records, count, 1, nullptr, d_orders, nullptr, d_results, d_peaks, nullptr,
                          nullptr, static_cast<cudaStream_t>(stream));
 }
 
@@ -571,7 +583,7 @@ dip_status dip_eval_orders(const dip_model *M, dip_workspace *w, const void *d_r
     if (!d_start != !d_end) return fail(DIP_EINVAL, "d_start and d_end go together");
     if (d_sel && !M->S) return fail(DIP_EINVAL, "a selection needs a strategy menu (dip_set_strategies)");
     if (M->device < 0 || !M->d_blob) return fail(DIP_EINVAL, "host-only model (cuda_device < 0)");
-    return launch_orders(M, w, d_records, count, false, d_orders, nullptr, d_sel, d_results, d_peaks, d_start, d_end,
+    return launch_orders(M, w, d_records, count, 0, d_orders, nullptr, d_sel, d_results, d_peaks, d_start, d_end,
                          static_cast<cudaStream_t>(stream));
 }
 
@@ -757,6 +769,101 @@ dip_status dip_eval_host(const dip_model *M, dip_workspace *w, const void *h_rec
         CUDA_TRY(cudaEventRecord(w->ev_free[b], sc));
     }
     CUDA_TRY(cudaEventRecord(w->ev_join, w->comp2));        // the argmin sees both streams' chunks
+    CUDA_TRY(cudaStreamWaitEvent(s, w->ev_join, 0));
+    w->last_results = nullptr;
+    w->last_count = count;
+    w->last_idx_bits = idx_bits;
+    w->last_fused = true;
+    return dip_argmin(M, w, count, shard_stride, rank, world, comm, out, stream);
+}
+
+// ---------------------------------------------------------------- device-mode encoding --
+static dipk::EncParams enc_params(const dip_model *M) {
+    dipk::EncParams p{};
+    p.P = M->P; p.nm = M->nmod; p.m = M->m; p.n_max = M->n_max; p.n_pad = M->n_pad; p.fbw = M->fbw;
+    p.stride = M->stride; p.off_nib = M->off_nib; p.off_fwd = M->off_fwd; p.off_bwd = M->off_bwd;
+    p.off_fb = M->off_fb; p.nsplit = M->nsplit;
+    for (uint32_t i = 0; i < M->nmod && i < 8; i++) {
+        if (M->max_split[i] > 1) p.maxsplit_gt1 |= 1u << i;
+        p.nib_slot[i] = M->nib_slot[i];
+    }
+    p.nbi = reinterpret_cast<const uint16_t *>(M->d_blob + M->kp.b_nbi);
+    return p;
+}
+
+dip_status dip_encode_candidates_device(const dip_model *M, const dip_candidate_batch *d, size_t count, void *d_out,
+                                        void *stream) {
+    if (!M || !d || (!d_out && count)) return fail(DIP_EINVAL, "null argument");
+    if (M->device < 0 || !M->d_blob) return fail(DIP_EINVAL, "host-only model (cuda_device < 0)");
+    if (!count) return DIP_OK;
+    if (!d->split || !d->n || !d->fwd_seq || !d->bwd_seq || !d->fb_bits) return fail(DIP_EINVAL, "null array");
+    dipk::EncParams p = enc_params(M);
+    p.split = d->split; p.n = d->n; p.fwd = d->fwd_seq; p.bwd = d->bwd_seq; p.fb = d->fb_bits;
+    p.out = static_cast<uint8_t *>(d_out);
+    p.count = count;
+    CUDA_TRY(dipk::launch_encode(p, M->num_sms, static_cast<cudaStream_t>(stream)));
+    g_launches++;
+    return DIP_OK;
+}
+
+// end to end from the HOST VIEW: per chunk, H2D of the candidates' arrays, the device encoder, the
+// scorer, the results D2H; copies of chunk c+1 overlap the encode + score of chunk c
+dip_status dip_eval_host_view(const dip_model *M, dip_workspace *w, const dip_candidate_batch *h, size_t count,
+                              dip_result *h_results, uint64_t shard_stride, uint32_t rank, uint32_t world,
+                              dip_comm *comm, dip_winner *out, void *stream) {
+    if (!M || !w || w->model != M || !out || (count && !h)) return fail(DIP_EINVAL, "null argument");
+    if (!w->host_chunk) return fail(DIP_EINVAL, "workspace has no host staging (host_chunk = 0)");
+    if (count && (!h->split || !h->n || !h->fwd_seq || !h->bwd_seq || !h->fb_bits)) return fail(DIP_EINVAL, "null array");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t idx_bits = bits_for(std::max<uint64_t>(count, 2));
+    if (!fused_ok(M, idx_bits)) return fail(DIP_ERANGE, "host path needs the fused argmin key (makespan bound too large)");
+    const size_t nq = (size_t)M->m * M->nmod, C = w->host_chunk;
+    // staging layout of one chunk: split [C][nq] | n [C] | fwd [C][n_max] | bwd [C][n_max] | fb [C][P][fbw]
+    auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+    const size_t o_n = up(C * nq), o_f = o_n + up(C * 4), o_b = o_f + up(C * 2 * M->n_max),
+                 o_fb = o_b + up(C * 2 * M->n_max), bytes = o_fb + up(C * 4ull * M->P * M->fbw);
+    for (int b = 0; b < dip_workspace::NBUF; b++)
+        if (!w->d_view[b]) CUDA_TRY(cudaMalloc(&w->d_view[b], bytes));
+    CUDA_TRY(cudaMemsetAsync(w->d_misc + 1, 0xFF, sizeof(unsigned long long), s));
+    const size_t Cc = std::min<size_t>(C, std::max<size_t>(8192, (count + 7) / 8));
+    const size_t nch = (count + Cc - 1) / Cc;
+    CUDA_TRY(cudaEventRecord(w->ev_start, s));
+    CUDA_TRY(cudaStreamWaitEvent(w->comp2, w->ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(w->copy_stream, w->ev_start, 0));
+    dipk::EncParams ep = enc_params(M);
+    for (size_t c = 0; c < nch; c++) {
+        const int b = (int)(c % dip_workspace::NBUF);
+        const bool odd = (c & 1) != 0;
+        cudaStream_t sc = odd ? w->comp2 : s;
+        const size_t lo = c * Cc, cnt = std::min(Cc, count - lo);
+        uint8_t *v = w->d_view[b];
+        if (c >= (size_t)dip_workspace::NBUF) CUDA_TRY(cudaStreamWaitEvent(w->copy_stream, w->ev_free[b], 0));
+        cudaStream_t cs = w->copy_stream;
+        CUDA_TRY(cudaMemcpyAsync(v, h->split + lo * nq, cnt * nq, cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaMemcpyAsync(v + o_n, h->n + lo, cnt * 4, cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaMemcpyAsync(v + o_f, h->fwd_seq + lo * M->n_max, cnt * 2 * M->n_max, cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaMemcpyAsync(v + o_b, h->bwd_seq + lo * M->n_max, cnt * 2 * M->n_max, cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaMemcpyAsync(v + o_fb, h->fb_bits + lo * (size_t)M->P * M->fbw, cnt * 4ull * M->P * M->fbw,
+                                 cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaEventRecord(w->ev_copied[b], cs));
+        CUDA_TRY(cudaStreamWaitEvent(sc, w->ev_copied[b], 0));
+        ep.split = v;
+        ep.n = reinterpret_cast<const uint32_t *>(v + o_n);
+        ep.fwd = reinterpret_cast<const uint16_t *>(v + o_f);
+        ep.bwd = reinterpret_cast<const uint16_t *>(v + o_b);
+        ep.fb = reinterpret_cast<const uint32_t *>(v + o_fb);
+        ep.out = w->d_rec[b];
+        ep.count = cnt;
+        CUDA_TRY(dipk::launch_encode(ep, M->num_sms, sc));
+        g_launches++;
+        dip_result *dres = w->d_res + b * C;
+        dip_status st = launch_chunk(M, w, w->d_rec[b], cnt, lo, idx_bits, true, dres, nullptr, sc, nullptr, nullptr,
+                                     odd ? w->d_spill2 : w->d_spill, w->d_misc + (odd ? 8 : 0));
+        if (st != DIP_OK) return st;
+        if (h_results) CUDA_TRY(cudaMemcpyAsync(h_results + lo, dres, cnt * sizeof(dip_result), cudaMemcpyDeviceToHost, sc));
+        CUDA_TRY(cudaEventRecord(w->ev_free[b], sc));
+    }
+    CUDA_TRY(cudaEventRecord(w->ev_join, w->comp2));
     CUDA_TRY(cudaStreamWaitEvent(s, w->ev_join, 0));
     w->last_results = nullptr;
     w->last_count = count;

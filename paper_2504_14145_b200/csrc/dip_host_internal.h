@@ -92,6 +92,9 @@ struct dip_workspace {
     cudaEvent_t ev_copied[NBUF] = {nullptr, nullptr, nullptr}, ev_free[NBUF] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_start = nullptr, ev_join = nullptr;
     unsigned long long *d_spill2 = nullptr;
+    // host-view path (dip_eval_host_view): NBUF device staging areas for the candidates' host-view
+    // arrays of one chunk (split | n | fwd | bwd | fb), allocated on first use
+    uint8_t *d_view[NBUF] = {nullptr, nullptr, nullptr};
 };
 
 struct dip_comm {

@@ -36,7 +36,7 @@ struct KParams {
     uint32_t g_seqF, g_seqB, g_posF, g_posB, g_depF0, g_depBP, g_ring, g_bmf, g_bytes;
     uint32_t warps_per_block, cpg;
     // per-schedule working set of the per-rank-order kernel (dip_order.cu), byte offsets in a group area
-    uint32_t o_row, o_seq, o_posof, o_sl, o_h, o_bm, o_mb, o_bytes;
+    uint32_t o_row, o_seq, o_posof, o_sl, o_h, o_bm, o_sum, o_mb, o_bytes;
     // per launch
     const uint8_t *records;
     uint8_t *records_out;       // non-null: interleave mode (f1) writes the F/B bit rows here
@@ -67,6 +67,20 @@ struct MCandParams {
     uint4 *ctab;                                        // out: [sum (w_max_i + 1)] x S
 };
 
+// device-mode encoding (dip_encode.cu): host-view arrays already on the device -> records
+struct EncParams {
+    const uint8_t *split;
+    const uint32_t *n;
+    const uint16_t *fwd, *bwd;
+    const uint32_t *fb;
+    const uint16_t *nbi;       // [m*nm] instances per (b, i) (the blob's copy)
+    uint8_t *out;
+    uint64_t count;
+    uint32_t P, nm, m, n_max, n_pad, fbw, stride, off_nib, off_fwd, off_bwd, off_fb, nsplit, maxsplit_gt1;
+    uint32_t nib_slot[8];
+};
+cudaError_t launch_encode(const EncParams &p, int num_sms, cudaStream_t s);
+
 cudaError_t launch_eval(const KParams &kp, int G, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_mcand(const MCandParams &p, cudaStream_t s);
 cudaError_t prepare_memopt(size_t smem);
@@ -75,7 +89,7 @@ cudaError_t launch_memopt(const KParams &kp, uint8_t *sel, uint32_t warp_bytes, 
 cudaError_t prepare_eval(int G, size_t smem);
 cudaError_t prepare_order(int G, size_t smem);
 cudaError_t occupancy_order(int G, int block, size_t smem, int *blocks_per_sm);
-cudaError_t launch_order(const KParams &kp, int G, bool build, int grid, int block, size_t smem, cudaStream_t s);
+cudaError_t launch_order(const KParams &kp, int G, int om, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t occupancy_eval(int G, int block, size_t smem, int *blocks_per_sm);
 cudaError_t launch_scan_argmin(const dip_result *res, uint64_t count, uint64_t index_base,
                                unsigned long long *mk_out, unsigned long long *idx_out, cudaStream_t s);

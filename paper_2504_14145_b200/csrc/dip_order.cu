@@ -101,8 +101,11 @@ __device__ __forceinline__ bool wrap_publish(uint64_t *slot, uint64_t value) {
 
 }  // namespace
 
-template <int G, bool BUILD>
+// OM: 0 = TIME of explicit per-rank orders, 1 = BUILD (f1), 2 = TIME of a record's own orders (its
+// shared sequences + F/B bit rows: the record scorer on per-segment state)
+template <int G, int OM>
 __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
+    constexpr bool BUILD = OM == 1;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t blob_bar;
     constexpr int CPG = 32 / G;
@@ -143,6 +146,8 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
     uint8_t *hB = hF + n_max;                                         //   B: from P-1 down)
     uint32_t *bmF = reinterpret_cast<uint32_t *>(ga + kp.o_bm);       // [P][nw] ready F positions (BUILD)
     uint32_t *bmB = bmF + P * nw;                                     // [P][nw] ready B positions
+    uint32_t *smF = reinterpret_cast<uint32_t *>(ga + kp.o_sum);      // [P] non-empty words of bmF rows
+    uint32_t *smB = smF + P;                                          // [P] ... of bmB rows
     uint8_t *Mb = ga + kp.o_mb;
     uint8_t *Pc = Mb + nq;
     uint8_t *Cc = Pc + nq;
@@ -195,7 +200,27 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
             Cc[q] = (uint8_t)cc;
         }
         __syncwarp();
-        if (BUILD) {
+        uint32_t wcur = 0, wnext = 0;
+        if (OM == 2 && laneOn) {   // the record's F/B bit row: exactly n ones in [0, 2n), zeros beyond
+            const uint32_t lim = 2 * n;
+            uint32_t ones = 0;
+            for (uint32_t w = 0; w < kp.fbw; w++) {
+                const uint32_t word = __ldg(reinterpret_cast<const uint32_t *>(rec + kp.off_fb) + w * P + r);
+                if (w == 0) wcur = word;
+                if (w == 1) wnext = word;
+                if (32 * w + 32 <= lim) {
+                    ones += __popc(word);
+                } else if (32 * w >= lim) {
+                    if (word) bad = true;
+                } else {
+                    const uint32_t msk = (1u << (lim - 32 * w)) - 1u;
+                    ones += __popc(word & msk);
+                    if (word & ~msk) bad = true;
+                }
+            }
+            if (ones != n) bad = true;
+        }
+        if (OM >= 1) {
             // priority orders: 16-byte loads; permutations of the present segment ids, 0xFFFF padding
             // (validation bitmaps: rank 0's and rank 1's rows of bmF, cleared again below)
             uint32_t *vF = bmF, *vB = bmB;
@@ -248,6 +273,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
         bad = (__ballot_sync(FULL, bad) & gmask) != 0;
         __syncwarp();
         for (uint32_t w = r; w < 2 * P * nw; w += G) bmF[w] = 0u;   // validation scratch -> ready sets
+        for (uint32_t w = r; w < 2 * P; w += G) smF[w] = 0u;
         __syncwarp();
 
         // ---------------- per-segment cost rows and state
@@ -268,6 +294,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                 if (BUILD && pf == 0) {      // no predecessor: ready on rank 0 from the start
                     const uint32_t p = pofF[s];
                     atomicOr(&bmF[p >> 5], 1u << (p & 31));
+                    atomicOr(&smF[0], 1u << (p >> 5));
                 }
             }
         }
@@ -280,79 +307,74 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
         uint16_t *ordOut = (BUILD && kp.orders_out && laneOn && gvalid)
                                ? kp.orders_out + (cand * P + r) * (uint64_t)(2 * n_max) : nullptr;
 
-        // publication of stage (d, s) on rank r ending at `end`: the next rank's input, or the
-        // wrap / join accumulators of the successor segments on the entry rank. Returns a bitmask
-        // of the lanes whose ready sets changed (BUILD sets the bits itself).
-        auto publish = [&](uint32_t d, uint32_t s, uint64_t end) -> uint32_t {
-            uint32_t touched = 0;
+        // publication of stage (d, s) on rank r ending at `end`: on an interior rank the next rank's
+        // ready time end + p2p goes into the segment's slot (BUILD: and the position into its ready
+        // set); on the exit rank the wrap / join accumulators of the successor segments on the entry
+        // rank (which add their own p2p). Returns the lanes whose ready sets changed through a wrap
+        // (they re-derive their minima); an interior publication is the single-stage ADD event `add`.
+        auto setbit = [&](uint32_t *bm, uint32_t *sm, uint32_t rr, uint32_t p) {
+            bm[rr * nw + (p >> 5)] |= 1u << (p & 31);
+            sm[rr] |= 1u << (p >> 5);
+        };
+        auto publish = [&](uint32_t d, uint32_t s, uint64_t end, uint64_t &addv) -> uint32_t {
+            uint32_t full = 0;
             if (d == 0) {
                 hF[s] = (uint8_t)(r + 1);
-                slF[s] = end;
                 if (!isLast) {
-                    if (BUILD) { const uint32_t p = pofF[s]; bmF[(r + 1) * nw + (p >> 5)] |= 1u << (p & 31); }
-                    touched |= 1u << (r + 1);
+                    addv = end + tab[rowx[s] & 0xFFFu].w;
+                    slF[s] = addv;
+                    if (BUILD) setbit(bmF, smF, r + 1, pofF[s]);
                 } else {
+                    slF[s] = end;
                     const uint32_t dc = segdec[s];
                     const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, k = (dc >> 15) & 0xFF, K = (dc >> 23) + 1;
                     const uint32_t w = tab[rowx[s] & 0xFFFu].w;
                     if (k + 1 < K) {
-                        if (wrap_publish(&slF[s + 1], end + w) && BUILD) {
-                            const uint32_t p = pofF[s + 1];
-                            bmF[p >> 5] |= 1u << (p & 31);
-                        }
-                        touched |= 1u;
+                        if (wrap_publish(&slF[s + 1], end + w) && BUILD) setbit(bmF, smF, 0, pofF[s + 1]);
+                        full |= 1u;
                     } else if (Cc[b * nmod + i]) {
                         for (uint32_t c = 0; c < nmod; c++) {
                             if (!((mi[i].cons_mask >> c) & 1u)) continue;
                             const uint32_t Mc = Mb[b * nmod + c];
                             for (uint32_t jc = 0; jc < Mc; jc++) {
                                 const uint32_t t2 = sbase[b * nmod + c] + jc * mi[c].K;
-                                if (wrap_publish(&slF[t2], end + w) && BUILD) {
-                                    const uint32_t p = pofF[t2];
-                                    bmF[p >> 5] |= 1u << (p & 31);
-                                }
+                                if (wrap_publish(&slF[t2], end + w) && BUILD) setbit(bmF, smF, 0, pofF[t2]);
                             }
                         }
-                        touched |= 1u;
+                        full |= 1u;
                     } else {                                   // loss turnaround (R-6)
-                        if (wrap_publish(&slB[s], end) && BUILD) {
-                            const uint32_t p = pofB[s];
-                            bmB[(P - 1) * nw + (p >> 5)] |= 1u << (p & 31);
-                        }
-                        touched |= 1u << (P - 1);
+                        if (wrap_publish(&slB[s], end) && BUILD) setbit(bmB, smB, P - 1, pofB[s]);
+                        full |= 1u << (P - 1);
                     }
                 }
             } else {
                 hB[s] = (uint8_t)(P - r);
-                slB[s] = end;
                 if (!isFirst) {
-                    if (BUILD) { const uint32_t p = pofB[s]; bmB[(r - 1) * nw + (p >> 5)] |= 1u << (p & 31); }
-                    touched |= 1u << (r - 1);
+                    addv = end + tab[rowx[s] & 0xFFFu].w;
+                    slB[s] = addv;
+                    if (BUILD) setbit(bmB, smB, r - 1, pofB[s]);
                 } else {
+                    slB[s] = end;
                     const uint32_t dc = segdec[s];
                     const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, k = (dc >> 15) & 0xFF;
                     if (k > 0) {                               // previous chunk, rank P-1 (+ its p2p)
-                        if (wrap_publish(&slB[s - 1], end + tab[rowx[s - 1] & 0xFFFu].w) && BUILD) {
-                            const uint32_t p = pofB[s - 1];
-                            bmB[(P - 1) * nw + (p >> 5)] |= 1u << (p & 31);
-                        }
+                        if (wrap_publish(&slB[s - 1], end + tab[rowx[s - 1] & 0xFFFu].w) && BUILD)
+                            setbit(bmB, smB, P - 1, pofB[s - 1]);
                     } else {                                   // producers' last chunks (+ their p2p)
                         for (uint32_t pm = 0; pm < nmod; pm++) {
                             if (!((mi[i].prod_mask >> pm) & 1u)) continue;
                             const uint32_t Mp = Mb[b * nmod + pm];
                             for (uint32_t jp = 0; jp < Mp; jp++) {
                                 const uint32_t t2 = sbase[b * nmod + pm] + jp * mi[pm].K + mi[pm].K - 1;
-                                if (wrap_publish(&slB[t2], end + tab[rowx[t2] & 0xFFFu].w) && BUILD) {
-                                    const uint32_t p = pofB[t2];
-                                    bmB[(P - 1) * nw + (p >> 5)] |= 1u << (p & 31);
-                                }
+                                if (wrap_publish(&slB[t2], end + tab[rowx[t2] & 0xFFFu].w) && BUILD)
+                                    setbit(bmB, smB, P - 1, pofB[t2]);
                             }
                         }
                     }
-                    touched |= 1u << (P - 1);
+                    full |= 1u << (P - 1);
                 }
             }
-            return touched;
+            return full;
         };
 
         if (BUILD) {
@@ -362,36 +384,42 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
             bool need = true;
             int last = -1;
             uint32_t fstep = 0;
-            // t_start of ready stage s on this rank
-            auto tsF = [&](uint32_t s) -> uint64_t {
-                return isFirst ? (slF[s] & VAL_MASK) : slF[s] + tab[rowx[s] & 0xFFFu].w;
-            };
-            auto tsB = [&](uint32_t s) -> uint64_t {
-                return isLast ? (slB[s] & VAL_MASK) : slB[s] + tab[rowx[s] & 0xFFFu].w;
-            };
             auto actOf = [&](uint32_t s) -> uint32_t {
                 const uint32_t e = rowx[s];
                 return (uint32_t)layers[(e >> 12) + r] * tab[e & 0xFFFu].z;
             };
+            // the largest activation of any of this rank's stages: below budget - it, no forward is gated
+            uint32_t maxact = 0;
+            if (laneOn && !bad)
+                for (uint32_t p = 0; p < n; p++) { const uint32_t a = actOf(seqF[p]); maxact = a > maxact ? a : maxact; }
+            const uint32_t *mF = bmF + (laneOn ? r : 0) * nw, *mB = bmB + (laneOn ? r : 0) * nw;
             for (;;) {
                 if (need && !done) {        // re-derive the queue minima from the ready bitmaps
                     tF = tG = tB = O_INF;
-                    const uint32_t *mF = bmF + r * nw, *mB = bmB + r * nw;
-                    for (uint32_t w = 0; w < nw; w++) {
+                    const bool nogate = cur + maxact <= bud;
+                    uint32_t ws = smF[r];
+                    while (ws) {
+                        const uint32_t w = __ffs(ws) - 1;
+                        ws &= ws - 1;
                         uint32_t bits = mF[w];
                         while (bits) {
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
                             const uint32_t s = seqF[p];
-                            const uint64_t t = tsF(s);
+                            const uint64_t t = slF[s] & VAL_MASK;
                             tG = t < tG ? t : tG;
-                            if (cur + actOf(s) <= bud) tF = t < tF ? t : tF;
+                            if (nogate || cur + actOf(s) <= bud) tF = t < tF ? t : tF;
                         }
-                        bits = mB[w];
+                    }
+                    ws = smB[r];
+                    while (ws) {
+                        const uint32_t w = __ffs(ws) - 1;
+                        ws &= ws - 1;
+                        uint32_t bits = mB[w];
                         while (bits) {
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
-                            const uint64_t t = tsB(seqB[p]);
+                            const uint64_t t = slB[seqB[p]] & VAL_MASK;
                             tB = t < tB ? t : tB;
                         }
                     }
@@ -409,7 +437,8 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     if (gk == O_INF && (alive & gmask)) { dl = true; done = true; }   // unreachable (acyclic)
                 }
                 __syncwarp();
-                uint32_t pl = 0xFFFFFFFFu, pdir = 0, psg = 0;
+                uint32_t pl = 0, ainfo = 0;
+                uint64_t addv = 0;
                 if (!done && gk != O_INF && (uint32_t)(gk & 31u) == (uint32_t)r) {
                     const uint64_t fmin = relax ? tG : tF, bmin = tB;
                     uint32_t dir;
@@ -418,26 +447,34 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     else if (bmin == O_INF) dir = 0u;
                     else dir = bmin <= fmin ? 1u : 0u;
                     const uint64_t td = dir ? bmin : fmin, lim = td > tlast ? td : tlast;
+                    const bool nogate = relax || cur + maxact <= bud;
                     // the highest-priority (lowest position) stage starting as early as possible
                     uint32_t *mrow = (dir ? bmB : bmF) + r * nw;
+                    uint32_t *msum = (dir ? smB : smF) + r;
                     const uint16_t *seq = dir ? seqB : seqF;
+                    const uint64_t *sl = dir ? slB : slF;
                     uint32_t s = 0, pos = 0;
                     uint64_t ts = 0;
+                    uint32_t ws = *msum;
                     bool found = false;
-                    for (uint32_t w = 0; w < nw && !found; w++) {
+                    while (ws && !found) {
+                        const uint32_t w = __ffs(ws) - 1;
+                        ws &= ws - 1;
                         uint32_t bits = mrow[w];
                         while (bits) {
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
                             const uint32_t sg = seq[p];
-                            const uint64_t t = dir ? tsB(sg) : tsF(sg);
+                            const uint64_t t = sl[sg] & VAL_MASK;
                             if (t > lim) continue;
-                            if (!dir && !relax && cur + actOf(sg) > bud) continue;
+                            if (!dir && !nogate && cur + actOf(sg) > bud) continue;
                             s = sg; pos = p; ts = t; found = true;
                             break;
                         }
                     }
-                    mrow[pos >> 5] &= ~(1u << (pos & 31));
+                    const uint32_t wrd = mrow[pos >> 5] & ~(1u << (pos & 31));
+                    mrow[pos >> 5] = wrd;
+                    if (!wrd) *msum &= ~(1u << (pos >> 5));
                     const uint32_t e = rowx[s];
                     const uint4 T = tab[e & 0xFFFu];
                     const uint32_t lay = layers[(e >> 12) + r];
@@ -452,42 +489,63 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     cnt++;
                     last = (int)dir;
                     done = cnt == S2;
-                    pl = publish(dir, s, end) | (1u << r);
-                    pdir = dir;
-                    psg = s;
+                    pl = publish(dir, s, end, addv) | (1u << r);
+                    // an interior publication adds ONE ready stage to a neighbour: (lane, dir, segment)
+                    if ((dir == 0 && !isLast) || (dir == 1 && !isFirst))
+                        ainfo = 1u | (dir << 1) | ((uint32_t)(dir ? r - 1 : r + 1) << 2) | (s << 8);
                 }
-                // which lanes must re-derive their minima: the placer and the lanes whose ready sets
-                // it changed (a whole-warp group shares the mask through one shuffle)
                 __syncwarp();
                 if constexpr (G == 32) {
+                    // the placer's news: lanes to re-derive (wraps, itself) and the single ADD event,
+                    // which its target folds into its minima in O(1)
                     const uint32_t who = (uint32_t)(gk & 31u);
-                    const uint32_t msk = gk != O_INF ? __shfl_sync(FULL, pl, (int)who) : 0u;
+                    const bool placed = gk != O_INF;
+                    const uint32_t msk = placed ? __shfl_sync(FULL, pl, (int)who) : 0u;
+                    const uint32_t ai = placed ? __shfl_sync(FULL, ainfo, (int)who) : 0u;
+                    const uint64_t av = placed ? __shfl_sync(FULL, addv, (int)who) : 0ull;
                     need = (msk >> r) & 1u;
+                    if ((ai & 1u) && ((ai >> 2) & 63u) == (uint32_t)r && !need && !done) {
+                        const uint32_t sa = ai >> 8;
+                        if (ai & 2u) {
+                            tB = av < tB ? av : tB;
+                        } else {
+                            tG = av < tG ? av : tG;
+                            if (cur + maxact <= bud || cur + actOf(sa) <= bud) tF = av < tF ? av : tF;
+                        }
+                    }
                 } else {
                     need = true;
                 }
-                (void)pdir; (void)psg;
             }
         } else {
-            // ---------------- TIME: lock-step longest path of explicit per-rank orders
-            const uint16_t *row = kp.orders_in + ((gvalid ? cand : 0) * P + (laneOn ? r : 0)) * (uint64_t)(2 * n_max);
+            // ---------------- TIME: lock-step longest path of explicit per-rank orders (OM 0) or of the
+            // record's shared sequences + F/B bits (OM 2)
+            const uint16_t *row = OM == 0 ? kp.orders_in + ((gvalid ? cand : 0) * P + (laneOn ? r : 0)) * (uint64_t)(2 * n_max)
+                                          : nullptr;
+            const uint32_t *wptr = reinterpret_cast<const uint32_t *>(rec + kp.off_fb) + 2 * P + r;   // word 2
             bool done = bad || !laneOn || n == 0;
             uint32_t rnd = 0;
             for (;;) {
-                const uint32_t e16 = done ? 0u : __ldg(&row[cnt]);
-                const uint32_t d = e16 >> 15, s = e16 & 0x7FFFu;
+                uint32_t d, s;
+                if constexpr (OM == 0) {
+                    const uint32_t e16 = done ? 0u : __ldg(&row[cnt]);
+                    d = e16 >> 15;
+                    s = e16 & 0x7FFFu;
+                } else {
+                    d = (wcur >> (cnt & 31)) & 1u;
+                    s = done ? 0u : (d ? seqB[bi] : seqF[fi]);
+                }
                 bool ready = false;
                 uint64_t dep = 0;
-                if (!done) {
-                    const uint32_t w = tab[rowx[s] & 0xFFFu].w;
+                if (!done) {   // the slot holds the ready time (end + p2p, or the wrap / join value)
                     if (d == 0) {
                         const uint64_t v = slF[s];
                         ready = isFirst ? (hF[s] == 0 && (v >> PEND_SHIFT) == 0) : hF[s] == (uint32_t)r;
-                        dep = isFirst ? v : v + w;
+                        dep = v;
                     } else {
                         const uint64_t v = slB[s];
                         ready = isLast ? (hB[s] == 0 && (v >> PEND_SHIFT) == 0) : hB[s] == P - 1 - (uint32_t)r;
-                        dep = isLast ? v : v + w;
+                        dep = v;
                     }
                 }
                 if ((++rnd & 7) == 0) {
@@ -519,17 +577,32 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     busy += lat;
                     cur = d ? cur - act : cur + act;
                     peak = cur > peak ? cur : peak;
-                    publish(d, s, end);
+                    uint64_t addv;
+                    publish(d, s, end, addv);
                     if (d) bi++; else fi++;
                     cnt++;
+                    if (OM == 2 && (cnt & 31) == 0) {      // next 32 F/B bits (the word after next prefetched)
+                        wcur = wnext;
+                        if (cnt + 32 < S2) wnext = __ldg(wptr);
+                        wptr += P;
+                    }
                     done = cnt == S2;
                 }
                 __syncwarp();
             }
             if (dl && laneOn) {   // deadlocked: finish the order-only memory scan (R-9)
                 while (cnt < S2) {
-                    const uint32_t e16 = __ldg(&row[cnt]);
-                    const uint32_t d = e16 >> 15, s = e16 & 0x7FFFu, e = rowx[s];
+                    uint32_t d, s;
+                    if constexpr (OM == 0) {
+                        const uint32_t e16 = __ldg(&row[cnt]);
+                        d = e16 >> 15;
+                        s = e16 & 0x7FFFu;
+                    } else {
+                        const uint32_t word = __ldg(reinterpret_cast<const uint32_t *>(rec + kp.off_fb) + (cnt >> 5) * P + r);
+                        d = (word >> (cnt & 31)) & 1u;
+                        s = d ? seqB[bi] : seqF[fi];
+                    }
+                    const uint32_t e = rowx[s];
                     uint32_t a = (uint32_t)layers[(e >> 12) + r] * tab[e & 0xFFFu].z;
                     if (kp.sel) {
                         const uint32_t idx = d ? bi : fi;
@@ -590,23 +663,24 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
 }
 
 template <int G>
-static const void *okfun(bool build) {
-    return build ? reinterpret_cast<const void *>(&dip_order_kernel<G, true>)
-                 : reinterpret_cast<const void *>(&dip_order_kernel<G, false>);
+static const void *okfun(int om) {
+    return om == 1 ? reinterpret_cast<const void *>(&dip_order_kernel<G, 1>)
+         : om == 2 ? reinterpret_cast<const void *>(&dip_order_kernel<G, 2>)
+                   : reinterpret_cast<const void *>(&dip_order_kernel<G, 0>);
 }
-static const void *order_kernel_for(int G, bool build) {
+static const void *order_kernel_for(int G, int om) {
     switch (G) {
-    case 4: return okfun<4>(build);
-    case 8: return okfun<8>(build);
-    case 16: return okfun<16>(build);
-    case 32: return okfun<32>(build);
+    case 4: return okfun<4>(om);
+    case 8: return okfun<8>(om);
+    case 16: return okfun<16>(om);
+    case 32: return okfun<32>(om);
     default: return nullptr;
     }
 }
 
 cudaError_t prepare_order(int G, size_t smem) {
-    for (int b = 0; b < 2; b++) {
-        const void *f = order_kernel_for(G, b != 0);
+    for (int b = 0; b < 3; b++) {
+        const void *f = order_kernel_for(G, b);
         if (!f) return cudaErrorInvalidValue;
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -616,8 +690,8 @@ cudaError_t prepare_order(int G, size_t smem) {
 
 cudaError_t occupancy_order(int G, int block, size_t smem, int *blocks_per_sm) {
     int best = 1 << 30;
-    for (int b = 0; b < 2; b++) {
-        const void *f = order_kernel_for(G, b != 0);
+    for (int b = 0; b < 3; b++) {
+        const void *f = order_kernel_for(G, b);
         if (!f) return cudaErrorInvalidValue;
         int x = 0;
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, f, block, smem);
@@ -629,17 +703,18 @@ cudaError_t occupancy_order(int G, int block, size_t smem, int *blocks_per_sm) {
 }
 
 template <int G>
-static void launch_og(const KParams &kp, bool build, int grid, int block, size_t smem, cudaStream_t s) {
-    if (build) dip_order_kernel<G, true><<<grid, block, smem, s>>>(kp);
-    else dip_order_kernel<G, false><<<grid, block, smem, s>>>(kp);
+static void launch_og(const KParams &kp, int om, int grid, int block, size_t smem, cudaStream_t s) {
+    if (om == 1) dip_order_kernel<G, 1><<<grid, block, smem, s>>>(kp);
+    else if (om == 2) dip_order_kernel<G, 2><<<grid, block, smem, s>>>(kp);
+    else dip_order_kernel<G, 0><<<grid, block, smem, s>>>(kp);
 }
 
-cudaError_t launch_order(const KParams &kp, int G, bool build, int grid, int block, size_t smem, cudaStream_t s) {
+cudaError_t launch_order(const KParams &kp, int G, int om, int grid, int block, size_t smem, cudaStream_t s) {
     switch (G) {
-    case 4: launch_og<4>(kp, build, grid, block, smem, s); break;
-    case 8: launch_og<8>(kp, build, grid, block, smem, s); break;
-    case 16: launch_og<16>(kp, build, grid, block, smem, s); break;
-    case 32: launch_og<32>(kp, build, grid, block, smem, s); break;
+    case 4: launch_og<4>(kp, om, grid, block, smem, s); break;
+    case 8: launch_og<8>(kp, om, grid, block, smem, s); break;
+    case 16: launch_og<16>(kp, om, grid, block, smem, s); break;
+    case 32: launch_og<32>(kp, om, grid, block, smem, s); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

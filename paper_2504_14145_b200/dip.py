@@ -108,6 +108,9 @@ def lib():
     L.dip_search.argtypes = [vp, vp, vp, ctypes.POINTER(_SearchParams), vp, vp, vp, ctypes.POINTER(_SearchResult), vp]
     L.dip_argmin.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp,
                              ctypes.POINTER(_Winner), vp]
+    L.dip_encode_candidates_device.argtypes = [vp, ctypes.POINTER(_CandBatch), ctypes.c_size_t, vp, vp]
+    L.dip_eval_host_view.argtypes = [vp, vp, ctypes.POINTER(_CandBatch), ctypes.c_size_t, vp, ctypes.c_uint64,
+                                     ctypes.c_uint32, ctypes.c_uint32, vp, ctypes.POINTER(_Winner), vp]
     L.dip_eval_host.argtypes = [vp, vp, vp, ctypes.c_size_t, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                 vp, ctypes.POINTER(_Winner), vp]
     L.dip_pack_key.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
@@ -122,6 +125,8 @@ def lib():
     L.dip_memopt.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
     L.dip_set_memopt_solver.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32]
     L.dip_memopt_stats.argtypes = [vp, vp, vp]
+    L.dip_ubench_int.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_double)]
     L.dip_comm_unique_id.argtypes = [vp]
     L.dip_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dip_comm_free.argtypes = [vp]
@@ -133,7 +138,7 @@ def lib():
               "dip_comm_unique_id", "dip_comm_init", "dip_comm_free", "dip_pack_key", "dip_unpack_key",
               "dip_timeline", "dip_compile_plan", "dip_validate_plan",
               "dip_set_strategies", "dip_strategy_candidates", "dip_memopt", "dip_set_memopt_solver",
-              "dip_memopt_stats"):
+              "dip_memopt_stats", "dip_ubench_int", "dip_encode_candidates_device", "dip_eval_host_view"):
         getattr(L, f).restype = st
     L.dip_launch_count.restype = ctypes.c_uint64
     L.dip_launch_count.argtypes = []
@@ -334,6 +339,19 @@ def memopt(model: Model, ws: Workspace, d_records, count: int, d_sel, d_results,
                             _ptr(d_results), _ptr(d_peaks), _stream(stream)), "dip_memopt")
 
 
+UBENCH_KINDS = ("IADD3", "VIMNMX", "ISETP+SEL", "SHFL+add", "IADD3+IADD3.X (u64 add)", "IMAD")
+
+
+def ubench_int(device: int = 0) -> dict:
+    """the integer-pipe microbenchmark: thread-level SASS instructions per second per kind"""
+    out = {}
+    for k, name in enumerate(UBENCH_KINDS):
+        v, ms = ctypes.c_double(), ctypes.c_double()
+        _check(lib().dip_ubench_int(k, device, ctypes.byref(v), ctypes.byref(ms)), "dip_ubench_int")
+        out[name] = v.value
+    return out
+
+
 def set_memopt_solver(model: Model, gap_permille: int = 50, node_cap: int = 4096):
     """f3: the per-rank ILP's relative optimality gap (per mille) and B&B child budget."""
     _check(lib().dip_set_memopt_solver(model.handle, gap_permille, node_cap), "dip_set_memopt_solver")
@@ -426,6 +444,32 @@ def eval_host(model: Model, ws: Workspace, h_records, count: int, h_results=None
     _check(lib().dip_eval_host(model.handle, ws.handle, _ptr(h_records), count, _ptr(h_results),
                                shard_stride if shard_stride is not None else count, rank, world,
                                comm.handle if comm else None, ctypes.byref(w), _stream(stream)), "dip_eval_host")
+    return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
+
+
+def _batch(arrs):
+    """the five host-view arrays (numpy arrays or tensors: split u8, n u32, fwd u16, bwd u16, fb u32)"""
+    return _CandBatch(*[_ptr(a) for a in arrs])
+
+
+def encode_device(model: Model, d_view, count: int, d_out, stream=None):
+    """§8(b) device mode: pack candidates whose host-view arrays (split, n, fwd, bwd, fb) are already
+    on the device (tensors) into device records d_out."""
+    cb = _batch(d_view)
+    _check(lib().dip_encode_candidates_device(model.handle, ctypes.byref(cb), count, _ptr(d_out), _stream(stream)),
+           "dip_encode_candidates_device")
+
+
+def eval_host_view(model: Model, ws: Workspace, h_view, count: int, h_results=None, shard_stride: Optional[int] = None,
+                   rank: int = 0, world: int = 1, comm: Optional[Comm] = None, stream=None) -> Winner:
+    """End to end from the candidates' host view (pinned split, n, fwd, bwd, fb arrays / tensors):
+    chunked H2D -> device encode -> scoring -> results D2H (h_results may be None) -> argmin."""
+    cb = _batch(h_view)
+    w = _Winner()
+    _check(lib().dip_eval_host_view(model.handle, ws.handle, ctypes.byref(cb), count, _ptr(h_results),
+                                    shard_stride if shard_stride is not None else count, rank, world,
+                                    comm.handle if comm else None, ctypes.byref(w), _stream(stream)),
+           "dip_eval_host_view")
     return Winner(bool(w.found), w.rank, w.global_index, w.makespan_ns)
 
 

@@ -66,3 +66,28 @@ def test_plan_one_batch(name, count):
     valid, D = dip.validate_plan(m, rec, acts, off)
     assert valid and np.array_equal(D, S)
     assert nmsg > 0 and len(off) == pb.P + 1
+
+
+@pytest.mark.parametrize("name,count", [("toy", 256), ("12B", 3000), ("T2V", 700)])
+def test_device_encode_and_host_view_pipeline(name, count):
+    """§8(b) device-mode encode: byte-identical records to the host encoder; dip_eval_host_view (host
+    view -> H2D -> device encode -> score -> results D2H -> argmin) == dip_eval_schedules on the
+    host-encoded records, results and winner"""
+    pb = gen.make_problem(name)
+    cs = gen.generate(pb, 0, count, mode=1 if name == "toy" else 0, p_mutate=0.2, p_bad=0.05)
+    m = dip.Model(pb, 0)
+    ws = dip.Workspace(m, host_chunk=1024)
+    s = torch.cuda.current_stream()
+    recs = m.encode(cs)
+    d_view = [torch.from_numpy(np.ascontiguousarray(getattr(cs, k))).cuda() for k in ("split", "n", "fwd", "bwd", "fb")]
+    d_out = torch.empty(count * m.stride, dtype=torch.uint8, device="cuda")
+    dip.encode_device(m, d_view, count, d_out, stream=s)
+    assert np.array_equal(d_out.cpu().numpy(), recs)
+    d_res = torch.empty(count * 24, dtype=torch.uint8, device="cuda")
+    dip.eval_schedules(m, ws, torch.from_numpy(recs).cuda(), count, d_res, None, stream=s)
+    win = dip.argmin(m, ws, count, stream=s)
+    h_view = [torch.from_numpy(np.ascontiguousarray(getattr(cs, k))).pin_memory() for k in ("split", "n", "fwd", "bwd", "fb")]
+    h_res = torch.empty(count * 24, dtype=torch.uint8).pin_memory()
+    w2 = dip.eval_host_view(m, ws, h_view, count, h_res, stream=s)
+    assert np.array_equal(h_res.numpy(), d_res.cpu().numpy())
+    assert (w2.found, w2.global_index, w2.makespan_ns) == (win.found, win.global_index, win.makespan_ns)
