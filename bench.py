@@ -465,7 +465,7 @@ def main():
                 tj = json.load(f)
             traffic = tj["dram_bytes_per_candidate"] * per
         issue = None
-        fp = os.path.join(ROOT, "profiles", f"r01_ncu_full_{args.config}.json")
+        fp = os.path.join(ROOT, "profiles", f"r02_ncu_full_{args.config}.json")
         if os.path.exists(fp):   # warp instructions per candidate from the same capture: the issue ceiling
             with open(fp) as f:
                 wi = json.load(f).get("warp_inst_per_candidate")
@@ -473,7 +473,7 @@ def main():
                 ach = wi * per / kern_s
                 pk = 4 * 148 * sm_max * 1e6
                 issue = {"achieved": ach / 1e12, "peak": pk / 1e12, "unit": "T warp-instr/s", "frac": ach / pk,
-                         "source": f"profiles/r01_ncu_full_{args.config}.json ({wi:.0f} warp instructions per candidate)"
+                         "source": f"profiles/r02_ncu_full_{args.config}.json ({wi:.0f} warp instructions per candidate)"
                                    " x candidates / kernel time vs 4 issue slots/clk/SM x 148 SMs x sm_max"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

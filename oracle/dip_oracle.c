@@ -1062,8 +1062,9 @@ int64_t oracle_argmin(const uint64_t *makespan, const uint32_t *status, uint64_t
  *          slack.
  *      M3b lower bound (the solver's relaxation bound, reading R-39): a Lagrangian relaxation of
  *          the memory constraints at the points K* where the warm start blocks a pair, with one
- *          multiplier mu found by bisection (fixed point 2^-16); every pair then picks its
- *          candidate independently and the bound is ceil(L(mu)), valid for any mu >= 0.
+ *          multiplier mu (fixed point 2^-16) bracketed by x16 steps and bisected to 1/64 relative
+ *          width; every pair then picks its candidate independently and the bound is ceil(L(mu))
+ *          at the better end of the bracket, valid for any mu >= 0.
  *      M3c branch and bound: if bound >= (1 - gap) * incumbent the incumbent is within the gap and
  *          is the answer; else depth-first over the pairs in forward order, each pair's candidates
  *          fastest first, a child skipped if it does not fit its points, a subtree entered only
@@ -1251,13 +1252,13 @@ static uint64_t ilp_bound(const ilp_t *I, uint32_t nfix) {
     if ((int64_t)D <= R) {
         out = ilp_L(I, nfix, cp, 0, R, fixed);
     } else {
-        for (int it = 0; it < 62; it++) {          /* D(hi) <= R: every pair at its least memory fits */
+        for (int it = 0; it < 16; it++) {          /* D(hi) <= R: every pair at its least memory fits */
             ilp_eval(I, nfix, cp, hi, &D, &V);
             if ((int64_t)D <= R) break;
             lo = hi;
-            hi *= 2;
+            hi *= 16;
         }
-        while (hi - lo > 1) {
+        while (hi - lo > 1 && hi - lo > (hi >> 6)) {    /* to 1/64 relative: any mu gives a valid bound */
             uint64_t mid = lo + (hi - lo) / 2;
             ilp_eval(I, nfix, cp, mid, &D, &V);
             if ((int64_t)D <= R) hi = mid; else lo = mid;

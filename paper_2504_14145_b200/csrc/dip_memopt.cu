@@ -100,8 +100,8 @@ __device__ __forceinline__ unsigned long long ilp_L(const uint4 *__restrict__ ct
 }
 
 // M3b: the Lagrangian bound with pairs < nfix fixed (their latency summed in `fixed`, their memory
-// taken out of R = sum over K* of (budget - fixed memory live there)); bisection on mu exactly as
-// the oracle's (same integer sequence, so the same bound)
+// taken out of R = sum over K* of (budget - fixed memory live there)); mu bracketed by x16 steps and
+// bisected to 1/64 relative width exactly as the oracle (same integer sequence, so the same bound)
 __device__ unsigned long long ilp_bound(const uint4 *__restrict__ ctab, const uint16_t *cbr, const uint8_t *cn,
                                         const uint32_t *cpa, uint32_t S, uint32_t n, uint32_t nfix, long long R,
                                         unsigned long long fixed) {
@@ -110,13 +110,13 @@ __device__ unsigned long long ilp_bound(const uint4 *__restrict__ ctab, const ui
     ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, 0ull, false, &D, &V);
     if ((long long)D <= R) return ilp_L(ctab, cbr, cn, cpa, S, n, nfix, 0ull, R, fixed);
     unsigned long long lo = 0, hi = 1;
-    for (int it = 0; it < 62; it++) {
+    for (int it = 0; it < 16; it++) {
         ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, hi, false, &D, &V);
         if ((long long)D <= R) break;
         lo = hi;
-        hi *= 2;
+        hi *= 16;
     }
-    while (hi - lo > 1) {
+    while (hi - lo > 1 && hi - lo > (hi >> 6)) {
         const unsigned long long mid = lo + (hi - lo) / 2;
         ilp_eval(ctab, cbr, cn, cpa, S, n, nfix, mid, false, &D, &V);
         if ((long long)D <= R) hi = mid; else lo = mid;

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
             // ---------------- f1: the dual-queue greedy, one stage per step
             bool done = bad || !laneOn || n == 0;
             uint64_t tF = O_INF, tG = O_INF, tB = O_INF;   // min t_start: ungated F, any F, B
-            bool need = true;
+            uint32_t need = 3;                             // bit 0: re-derive t_fw / t_gated, bit 1: t_bw
             int last = -1;
             uint32_t fstep = 0;
             auto actOf = [&](uint32_t s) -> uint32_t {
@@ -394,8 +394,8 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                 for (uint32_t p = 0; p < n; p++) { const uint32_t a = actOf(seqF[p]); maxact = a > maxact ? a : maxact; }
             const uint32_t *mF = bmF + (laneOn ? r : 0) * nw, *mB = bmB + (laneOn ? r : 0) * nw;
             for (;;) {
-                if (need && !done) {        // re-derive the queue minima from the ready bitmaps
-                    tF = tG = tB = O_INF;
+                if ((need & 1u) && !done) {        // re-derive the queue minima from the ready bitmaps
+                    tF = tG = O_INF;
                     const bool nogate = cur + maxact <= bud;
                     uint32_t ws = smF[r];
                     while (ws) {
@@ -411,7 +411,10 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                             if (nogate || cur + actOf(s) <= bud) tF = t < tF ? t : tF;
                         }
                     }
-                    ws = smB[r];
+                }
+                if ((need & 2u) && !done) {
+                    tB = O_INF;
+                    uint32_t ws = smB[r];
                     while (ws) {
                         const uint32_t w = __ffs(ws) - 1;
                         ws &= ws - 1;
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     if (gk == O_INF && (alive & gmask)) { dl = true; done = true; }   // unreachable (acyclic)
                 }
                 __syncwarp();
-                uint32_t pl = 0, ainfo = 0;
+                uint32_t pl = 0, ainfo = 0, selfneed = 0;
                 uint64_t addv = 0;
                 if (!done && gk != O_INF && (uint32_t)(gk & 31u) == (uint32_t)r) {
                     const uint64_t fmin = relax ? tG : tF, bmin = tB;
@@ -489,7 +492,12 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     cnt++;
                     last = (int)dir;
                     done = cnt == S2;
-                    pl = publish(dir, s, end, addv) | (1u << r);
+                    pl = publish(dir, s, end, addv);
+                    // the placer's own minima: its placed direction lost a stage; a backward placement
+                    // also lowered its memory, which can only un-gate forwards (none gated: t_fw = t_gated)
+                    if (dir == 0) selfneed = 1u;
+                    else if (cur + maxact <= bud) { selfneed = 2u; tF = tG; }
+                    else selfneed = 3u;
                     // an interior publication adds ONE ready stage to a neighbour: (lane, dir, segment)
                     if ((dir == 0 && !isLast) || (dir == 1 && !isFirst))
                         ainfo = 1u | (dir << 1) | ((uint32_t)(dir ? r - 1 : r + 1) << 2) | (s << 8);
@@ -503,18 +511,18 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     const uint32_t msk = placed ? __shfl_sync(FULL, pl, (int)who) : 0u;
                     const uint32_t ai = placed ? __shfl_sync(FULL, ainfo, (int)who) : 0u;
                     const uint64_t av = placed ? __shfl_sync(FULL, addv, (int)who) : 0ull;
-                    need = (msk >> r) & 1u;
-                    if ((ai & 1u) && ((ai >> 2) & 63u) == (uint32_t)r && !need && !done) {
+                    need = (((msk >> r) & 1u) ? 3u : 0u) | selfneed;
+                    if ((ai & 1u) && ((ai >> 2) & 63u) == (uint32_t)r && !done) {
                         const uint32_t sa = ai >> 8;
                         if (ai & 2u) {
-                            tB = av < tB ? av : tB;
-                        } else {
+                            if (!(need & 2u)) tB = av < tB ? av : tB;
+                        } else if (!(need & 1u)) {
                             tG = av < tG ? av : tG;
                             if (cur + maxact <= bud || cur + actOf(sa) <= bud) tF = av < tF ? av : tF;
                         }
                     }
                 } else {
-                    need = true;
+                    need = 3u;
                 }
             }
         } else {
