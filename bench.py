@@ -435,6 +435,19 @@ def main():
                   "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"],
                   "same_split_template_fixed_order_ns": int(res["makespan_ns"][0]),
                   "same_split_template_f1_ns": int(f1_first["makespan_ns"]) if f1_first is not None else None}
+            # the paper's search-efficiency comparison: the same budget, rollout stream and
+            # scorer with random exploration and with depth-first search instead of MCTS
+            cmp = {}
+            for pol, nm in ((1, "random"), (2, "dfs")):
+                t0 = time.perf_counter()
+                sp = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,
+                                rollouts=args.f2_rollouts, alpha=1.0, beta=0.5, stream=stream, policy=pol)
+                cmp[nm] = {"best_makespan_ns": sp["makespan"], "best_score": sp["score"],
+                           "trace": [round(float(v), 6) for v in sp["trace"]],
+                           "rollouts_per_s": sp["scored"] / (time.perf_counter() - t0)}
+            cmp["mcts"] = {"best_makespan_ns": sr["makespan"], "best_score": sr["score"],
+                           "trace": [round(float(v), 6) for v in sr["trace"]]}
+            f2["policy_comparison"] = cmp
             if world == 1 and not args.no_cpu_baseline:   # the oracle's search (single-threaded), 1 round x 64 leaves
                 import oracle
                 t0 = time.perf_counter()

@@ -269,6 +269,10 @@ typedef struct {
     double alpha, beta;       /* UCB hyper-parameters */
     int32_t memopt;           /* nonzero: score each rollout after dip_memopt (f3); needs
                                  dip_set_strategies; the score's LB stays the base-table bound */
+    int32_t policy;           /* 0 = MCTS; the paper's comparison variants: 1 = random
+                                 exploration (every rollout a uniformly random sequence from the root),
+                                 2 = depth-first search (pre-order over the sequence tree, children
+                                 in class order); rollouts / scoring / backpropagation unchanged */
 } dip_search_params;
 
 typedef struct {

@@ -71,7 +71,7 @@ def _load():
         lib.oracle_search.argtypes = [ctypes.POINTER(_OProblem), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
                                       ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                       ctypes.c_double, ctypes.c_double] + [ctypes.c_void_p] * 7 + \
-            [ctypes.c_uint32] + [ctypes.c_void_p] * 3 + [ctypes.c_uint32]
+            [ctypes.c_uint32] + [ctypes.c_void_p] * 3 + [ctypes.c_uint32, ctypes.c_uint32]
         lib.oracle_mem_candidates.restype = ctypes.c_int
         lib.oracle_mem_candidates.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 3 + [ctypes.c_uint32] * 2 + \
             [ctypes.c_void_p]
@@ -81,7 +81,7 @@ def _load():
             [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
         lib.oracle_mcts_table.restype = ctypes.c_uint32
         lib.oracle_mcts_table.argtypes = [ctypes.c_uint32, ctypes.c_uint64] + [ctypes.c_uint32] * 3 + \
-            [ctypes.c_double] * 2 + [ctypes.c_void_p] * 7
+            [ctypes.c_double] * 2 + [ctypes.c_void_p] * 7 + [ctypes.c_uint32]
         lib.oracle_select_rank.restype = ctypes.c_int
         lib.oracle_select_rank.argtypes = [ctypes.c_uint32] + [ctypes.c_void_p] * 4 + \
             [ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]
@@ -175,9 +175,11 @@ def interleave(pb, cands, first: int = 0, count: Optional[int] = None, threads: 
     return ords, res
 
 
-def mcts_table(Cn: int, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float, beta: float, table):
+def mcts_table(Cn: int, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float, beta: float, table,
+               policy: int = 0):
     """S4-S6 alone with rollouts scored by table[seq[0], seq[1]] (a test fixture):
-    returns dict(trace [rounds], leaves [rounds, leaves] node ids, tree: parent, cls, N, s per node)."""
+    returns dict(trace [rounds], leaves [rounds, leaves] node ids, tree: parent, cls, N, s per node).
+    policy: 0 MCTS, 1 random exploration, 2 depth-first (P:963-972's comparison)."""
     t = np.ascontiguousarray(np.asarray(table, np.float64).reshape(-1))
     assert t.size == Cn * Cn
     cap = 1 + rounds * leaves
@@ -187,15 +189,16 @@ def mcts_table(Cn: int, seed: int, rounds: int, leaves: int, rollouts: int, alph
     lib = _load()
     nn = lib.oracle_mcts_table(Cn, seed & ((1 << 64) - 1), rounds, leaves, rollouts, alpha, beta, t.ctypes.data,
                                trace.ctypes.data, lv.ctypes.data, par.ctypes.data, cls.ctypes.data, N.ctypes.data,
-                               sv.ctypes.data)
+                               sv.ctypes.data, policy)
     return dict(trace=trace, leaves=lv, parent=par[:nn], cls=cls[:nn], N=N[:nn], s=sv[:nn])
 
 
 def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha: float = 1.0, beta: float = 0.5,
-           menu=None, S: int = 10):
+           menu=None, S: int = 10, policy: int = 0):
     """S1-S6: MCTS over class orders with batched rounds, scoring rollouts with I1-I6
-    (then M1-M4 if a strategy menu (f, b, act) is given). Returns dict(score, makespan, trace, fwd,
-    bwd, bits, scored)."""
+    (then M1-M4 if a strategy menu (f, b, act) is given); policy 1 / 2 = the random / depth-first
+    exploration the paper compares against. Returns dict(score, makespan, trace, fwd,
+    bwd, orders, scored)."""
     from gen import Candidates
     lib = _load()
     dummy = Candidates(pb, 1)
@@ -211,7 +214,7 @@ def search(pb, split, seed: int, rounds: int, leaves: int, rollouts: int, alpha:
     arrs = _menu_arrays(menu)                     # kept alive for the call
     lib.oracle_search(ctypes.byref(bd.pb), pb.n_max, pb.fbw, sp.ctypes.data, seed & ((1 << 64) - 1), rounds, leaves,
                       rollouts, alpha, beta, trace.ctypes.data, ctypes.byref(sc), ctypes.byref(mk), fwd.ctypes.data,
-                      bwd.ctypes.data, ords.ctypes.data, ctypes.byref(scored), *_menu_args(arrs, S))
+                      bwd.ctypes.data, ords.ctypes.data, ctypes.byref(scored), *_menu_args(arrs, S), policy)
     return dict(score=sc.value, makespan=mk.value, trace=trace, fwd=fwd, bwd=bwd, orders=ords, scored=scored.value)
 
 

@@ -801,10 +801,15 @@ static void s_order(const oproblem *pb, const uint8_t *split, const uint32_t *ba
  * optional outputs: trace [rounds] best score after each round, leaves_out [rounds][leaves] the
  * selected / expanded leaf of every slot, the tree (parent, class, N, s) of every node. */
 typedef void (*mcts_score_fn)(void *ctx, uint32_t count, const uint32_t *seqs, const int *owner, double *scores);
+/* policy (the paper's search-efficiency comparison): 0 = MCTS (UCB selection, S4-S5);
+ * 1 = random exploration (every leaf is the root: all rollouts are uniformly random sequences);
+ * 2 = depth-first search (the leaf is the next node of a pre-order traversal of the sequence tree,
+ * children in class order: expand the previous leaf if it is incomplete, else its nearest ancestor
+ * with an unexpanded child). Rollouts, scoring and backpropagation are the same for all three. */
 static uint32_t mcts_run(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t leaves, uint32_t rollouts,
                          double alpha, double beta, mcts_score_fn score, void *ctx, double *trace,
                          int32_t *leaves_out, int32_t *t_parent, int32_t *t_cls, uint32_t *t_N, double *t_s,
-                         uint64_t *scored_out) {
+                         uint64_t *scored_out, uint32_t policy) {
     uint32_t ncap = 1 + rounds * leaves, nn = 1;
     snode *T = calloc(ncap, sizeof(snode));
     T[0].parent = -1; T[0].cls = -1; T[0].depth = 0;
@@ -816,13 +821,20 @@ static uint32_t mcts_run(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t l
     uint8_t *used = malloc(Cn);
     double best = -1.0;
     uint64_t u = 0;
+    int dfs_cur = 0;
     *scored_out = 0;
     for (uint32_t rd = 0; rd < rounds; rd++) {
         uint32_t cnt = 0;
         for (uint32_t l = 0; l < leaves; l++) {
             int v = 0;
             memset(used, 0, Cn);
-            for (;;) {                                           /* S4 / S5 */
+            if (policy == 2) {                                   /* DFS: climb from the previous leaf */
+                v = dfs_cur;
+                while (v > 0 && (uint32_t)T[v].nch >= Cn - (uint32_t)T[v].depth) v = T[v].parent;
+                if (v == 0 && (uint32_t)T[0].nch >= Cn) v = dfs_cur;   /* the whole tree is explored */
+                for (int x = v; x > 0; x = T[x].parent) used[T[x].cls] = 1;
+            }
+            for (; policy != 1;) {                               /* S4 / S5 (random: the root) */
                 snode *nd = &T[v];
                 if ((uint32_t)nd->depth == Cn) break;
                 if ((uint32_t)nd->nch < Cn - nd->depth) {        /* S5: the next unused class */
@@ -836,6 +848,7 @@ static uint32_t mcts_run(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t l
                     v = id;
                     break;
                 }
+                if (policy == 2) break;                          /* DFS: a complete leaf again */
                 double Nx = (double)(nd->N + nd->vl), bu = -1.0;   /* S4: UCB */
                 int bc = -1;
                 for (int x = 0; x < nd->nch; x++) {
@@ -849,6 +862,7 @@ static uint32_t mcts_run(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t l
             }
             for (int x = v; x >= 0; x = T[x].parent) T[x].vl++;
             leaf[l] = v;
+            dfs_cur = v;
             if (leaves_out) leaves_out[rd * leaves + l] = v;
             uint32_t d = (uint32_t)T[v].depth;
             for (int x = v; x > 0; x = T[x].parent) seq[T[x].depth - 1] = (uint32_t)T[x].cls;
@@ -913,11 +927,11 @@ static void tab_score(void *ctx, uint32_t count, const uint32_t *seqs, const int
 }
 uint32_t oracle_mcts_table(uint32_t Cn, uint64_t seed, uint32_t rounds, uint32_t leaves, uint32_t rollouts,
                            double alpha, double beta, const double *table, double *trace, int32_t *leaves_out,
-                           int32_t *t_parent, int32_t *t_cls, uint32_t *t_N, double *t_s) {
+                           int32_t *t_parent, int32_t *t_cls, uint32_t *t_N, double *t_s, uint32_t policy) {
     tab_ctx c = {Cn, table};
     uint64_t scored;
     return mcts_run(Cn, seed, rounds, leaves, rollouts, alpha, beta, tab_score, &c, trace, leaves_out, t_parent,
-                    t_cls, t_N, t_s, &scored);
+                    t_cls, t_N, t_s, &scored, policy);
 }
 
 /* S1-S3 for oracle_search: a class sequence -> priority orders (S2) -> interleaving (I1-I6, orders)
@@ -980,7 +994,8 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
                   uint32_t rounds, uint32_t leaves, uint32_t rollouts, double alpha, double beta,
                   double *trace, double *best_score, uint64_t *best_makespan, uint16_t *best_fwd,
                   uint16_t *best_bwd, uint16_t *best_ord /* [P][2 n_max] */, uint64_t *scored_out,
-                  uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma, uint32_t S) {
+                  uint32_t n_strat, const uint32_t *mf, const uint32_t *mb, const uint32_t *ma, uint32_t S,
+                  uint32_t policy) {
     omenu mn = {n_strat, S, mf, mb, ma, 50, 4096};   /* n_strat = 0: rollouts are interleaved only */
     const uint32_t P = pb->P, nm = pb->nmod, m = pb->m;
     uint32_t *base = malloc(sizeof(uint32_t) * (m * nm + 1));
@@ -1019,7 +1034,7 @@ int oracle_search(const oproblem *pb, uint32_t n_max, uint32_t fbw, const uint8_
     }
     srch_ctx c = {pb, &mn, n_max, fbw, n, C, Cn, split, base, clsof, LB, -1.0, best_makespan, best_fwd, best_bwd, best_ord};
     mcts_run(Cn, seed, rounds, leaves, rollouts, alpha, beta, search_score, &c, trace, NULL, NULL, NULL, NULL, NULL,
-             scored_out);
+             scored_out, policy);
     *best_score = c.best > 0.0 ? c.best : 0.0;
     if (!(c.best > 0.0)) *best_makespan = UINT64_MAX;     /* no feasible (status OK) rollout */
     free(base); free(clsof);

@@ -227,6 +227,9 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     const bool prof = std::getenv("DIP_SEARCH_PROFILE") != nullptr;   // per-phase wall times to stderr
     double t_sel = 0, t_build = 0, t_gpu = 0, t_back = 0;
     auto now = []() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    if (prm->policy < 0 || prm->policy > 2) { cudaFree(d_rec); cudaFree(d_res); cudaFree(d_ord); if (d_sel) cudaFree(d_sel);
+        return fail(DIP_EINVAL, "policy must be 0 (MCTS), 1 (random) or 2 (DFS)"); }
+    int dfs_cur = 0;
     for (; rd < prm->rounds; rd++) {
         double t0 = now();
         // ---- selection + expansion of B leaves (virtual visits keep the batch diverse)
@@ -237,7 +240,13 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
         for (uint32_t l = 0; l < B; l++) {
             int v = 0;
             std::vector<char> used(S.Cn, 0);
-            for (;;) {
+            if (prm->policy == 2) {   // DFS: from the previous leaf, up to the nearest node with an unexpanded child
+                v = dfs_cur;
+                while (v > 0 && tree[v].children.size() >= S.Cn - (uint32_t)tree[v].depth) v = tree[v].parent;
+                if (v == 0 && tree[0].children.size() >= S.Cn) v = dfs_cur;   // the whole tree is explored
+                for (int x = v; x > 0; x = tree[x].parent) used[tree[x].cls] = 1;
+            }
+            for (; prm->policy != 1;) {   // (random exploration: the root)
                 Node &nd = tree[v];
                 if ((uint32_t)nd.depth == S.Cn) break;
                 const uint32_t remaining = S.Cn - nd.depth;
@@ -256,6 +265,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
                     v = id;
                     break;
                 }
+                if (prm->policy == 2) break;                    // DFS: a complete leaf again
                 const double Nx = (double)(nd.N + nd.vloss), lnNx = std::log(Nx);
                 const bool a1 = prm->alpha == 1.0;       // pow(s, 1) is s exactly: skip the call
                 int bestc = -1;
@@ -271,6 +281,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
             }
             for (int x = v; x >= 0; x = tree[x].parent) tree[x].vloss++;
             leaf[l] = v;
+            dfs_cur = v;
             // the fixed prefix; its R uniformly random completions (one for a complete sequence) are
             // drawn by the record-building threads below, each from its own counter-based stream
             std::vector<uint32_t> prefix;

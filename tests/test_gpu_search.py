@@ -67,3 +67,18 @@ def test_search_beats_templates_on_94B_winner_split():
     assert g["found"] and g["makespan"] <= int(tf1.makespan[0]) < int(fixed.makespan[0])
     print(f"RESULT f2 94B winner split: search {g['makespan']} ns, template f1 {int(tf1.makespan[0])} ns, "
           f"template fixed order {int(fixed.makespan[0])} ns")
+
+
+@pytest.mark.parametrize("name,policy", [("toy", 1), ("toy", 2), ("12B", 1), ("12B", 2)])
+def test_exploration_policies_match_oracle_trajectory(name, policy):
+    """the paper's comparison variants: random exploration and depth-first search take the
+    oracle's trajectory exactly (same rollout stream, same scorer)"""
+    pb = gen.make_problem(name)
+    cs = gen.generate(pb, 0, 1, mode=1 if name == "toy" else 0, p_mutate=0, p_bad=0)
+    m = dip.Model(pb, 0)
+    ws = dip.Workspace(m)
+    g = dip.search(m, ws, cs.split[0], seed=7, rounds=6, leaves=8, rollouts=4, policy=policy,
+                   stream=torch.cuda.current_stream())
+    o = oracle.search(pb, cs.split[0], seed=7, rounds=6, leaves=8, rollouts=4, policy=policy)
+    assert np.array_equal(g["trace"], o["trace"]) and g["makespan"] == o["makespan"]
+    assert np.array_equal(g["orders"], o["orders"]) and g["scored"] == o["scored"]

@@ -204,3 +204,40 @@ def test_tree_policy_deeper_scores():
     for x, (p, c, n, v) in enumerate(tr):
         if p >= 0:
             assert tr[p][3] >= v and tr[p][2] >= n
+
+
+def _path(t, v):
+    out = []
+    while v > 0:
+        out.append(int(t["cls"][v]))
+        v = int(t["parent"][v])
+    return tuple(out[::-1])
+
+
+def test_depth_first_policy_is_pre_order():
+    """P:963-972's DFS variant: the leaves follow a pre-order traversal of the sequence tree with
+    children in class order (written out by hand for Cn = 3)"""
+    t = oracle.mcts_table(3, seed=1, rounds=13, leaves=1, rollouts=2, alpha=1.0, beta=0.5,
+                          table=[[0.5] * 3, [0.8] * 3, [0.7] * 3], policy=2)
+    assert [_path(t, int(v)) for v in t["leaves"][:, 0]] == [
+        (0,), (0, 1), (0, 1, 2), (0, 2), (0, 2, 1), (1,), (1, 0), (1, 0, 2), (1, 2), (1, 2, 0), (2,), (2, 0), (2, 0, 1)]
+
+
+def test_random_policy_never_builds_a_tree():
+    """P:963-972's random-exploration variant: every rollout is a uniformly random sequence from the
+    root; the root is the only node and counts every leaf slot"""
+    t = oracle.mcts_table(3, seed=1, rounds=5, leaves=2, rollouts=2, alpha=1.0, beta=0.5,
+                          table=[[0.5] * 3, [0.8] * 3, [0.7] * 3], policy=1)
+    assert t["leaves"].tolist() == [[0, 0]] * 5 and t["N"].tolist() == [10] and len(t["parent"]) == 1
+
+
+def test_policies_share_the_rollout_stream():
+    """the three policies draw the same rollout counter stream: at equal budget the random policy's
+    best is the best of the same number of uniformly random sequences, never above the exhaustive
+    optimum, and MCTS's exhaustive-budget optimum is reached"""
+    pb = tiny_problem()
+    split = np.ones(3, np.uint8)
+    best_score, best_mk = brute_force(pb, split)
+    for pol in (1, 2):
+        r = oracle.search(pb, split, seed=11, rounds=40, leaves=2, rollouts=4, policy=pol)
+        assert r["score"] <= best_score and r["makespan"] >= best_mk and (np.diff(r["trace"]) >= 0).all()
