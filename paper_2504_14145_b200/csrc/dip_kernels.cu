@@ -368,11 +368,21 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             const uint32_t d = (wcur >> (t & 31)) & 1u;            // 0 = F, 1 = B
             const bool wrapC = (wrapBits >> d) & 1u;
             const bool wrapP = (wrapPub >> d) & 1u;
+#ifdef DIP_PACKCNT   // A/B: the F and B counts in one word, two shuffles
+            const uint32_t cFB = cF | (cB << 16);
+            const uint32_t up = __shfl_up_sync(FULL, cFB, 1, G), dn = __shfl_down_sync(FULL, cFB, 1, G);
+            const uint32_t fu = up & 0xFFFFu, bu = up >> 16, fd = dn & 0xFFFFu, bd = dn >> 16;
+#else
             const uint32_t fu = __shfl_up_sync(FULL, cF, 1, G), bu = __shfl_up_sync(FULL, cB, 1, G);
             const uint32_t fd = __shfl_down_sync(FULL, cF, 1, G), bd = __shfl_down_sync(FULL, cB, 1, G);
+#endif
             const uint32_t idx = d ? cB : cF;
             const uint32_t nb = wrapC ? 0xFFFFu : (d ? bd : fu);                        // producer's count
+#ifdef DIP_CLAMPROW  // A/B: done lanes read a clamped (in-range, unused) row instead of a select
+            const uint2 e = posAll[d * n_max + min(idx, n_max - 1)];
+#else
             const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];       // done lanes: a safe row
+#endif
             const uint32_t ring = (idx & (D - 1)) * P;
             const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (d ? colIn1 : colIn0)];
             uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)] : &ringAll[ring + (d ? colOut1 : colOut0)];

@@ -112,6 +112,19 @@ extern "C" dip_status dip_set_strategies(dip_model *M, uint32_t n_strat, const u
             }
         }
     }
+    {   // the makespan bound of f3's re-timing: a selected candidate's stage latency may exceed the
+        // base tables' (a menu whose strategy 0 is not the base scheme), so the fused argmin key's
+        // packing and the 2^53 bubble guard are re-checked with the candidate table's largest stage
+        uint64_t maxc = 0, maxp2p = 0;
+        for (size_t x = 0; x < h.size(); x++) maxc = std::max<uint64_t>(maxc, std::max(h[x].x, h[x].y));
+        for (size_t t = 0; t + 3 < M->tab.size(); t += 4) maxp2p = std::max<uint64_t>(maxp2p, M->tab[t + 3]);
+        const unsigned __int128 b3 = (unsigned __int128)P * 2ull * M->n_max * (maxc + maxp2p);
+        if (b3 * P >= ((unsigned __int128)1 << 53)) {
+            cudaFree(d_ctab); cudaFree(d_crow);
+            return fail(DIP_ERANGE, "makespan bound with the strategy candidates exceeds 2^53 / P");
+        }
+        if ((uint64_t)b3 > M->mk_bound) M->mk_bound = (uint64_t)b3;
+    }
     {   // the selection keeps slack in int32: budget and the live memory must stay below 2^31 KiB
         uint64_t maxmem = 0, maxbud = 0;
         for (size_t x = 0; x < h.size(); x++) maxmem = std::max<uint64_t>(maxmem, h[x].z);

@@ -222,6 +222,13 @@ class Model:
         self.fbw = inf.fbw
         self.stride = inf.record_stride
 
+    def refresh_info(self) -> dict:
+        """re-read dip_model_get_info (dip_set_strategies may raise the makespan bound)"""
+        inf = _ModelInfo()
+        _check(lib().dip_model_get_info(self.handle, ctypes.byref(inf)), "dip_model_get_info")
+        self.info = {k: getattr(inf, k) for k, _ in _ModelInfo._fields_}
+        return self.info
+
     def encode(self, cands, out=None, threads: int = 0):
         """Pack host-view candidates (split, n, fwd, bwd, fb arrays) into records; returns `out`
         (a numpy uint8 array, or the given numpy array / pinned torch tensor)."""

@@ -111,11 +111,11 @@ def test_memopt_parity_other_S(S):
 
 
 def test_memopt_bench_size_sampled():
-    # the bench's f3 launch shape: 16,384 94B schedules in one call, 256 sampled against the oracle
+    # the bench's f3 launch shape: 16,384 94B schedules in one call, 1,024 sampled against the oracle
     pb = gen.make_problem("94B")
     cs = gen.generate(pb, 0, 16384, threads=16)
     idx = np.unique(np.concatenate([[0, 1, 2, 4095, 4096, 8191, 16382, 16383],
-                                    np.random.default_rng(5).choice(16384, 248, replace=False)]))
+                                    np.random.default_rng(5).choice(16384, 1016, replace=False)]))
     check(pb, cs, idx=idx)
 
 
@@ -210,3 +210,18 @@ def test_memopt_on_interleaved_orders(name, count):
     assert np.array_equal(d_pk.cpu().numpy().view(np.uint32).astype(np.uint64), ref.peaks)
     if name != "toy":
         assert sel[good].any()
+
+
+def test_strategy_menu_raises_the_makespan_bound():
+    """a menu whose candidates are slower than the base tables must raise the model's
+    makespan bound (the fused argmin key's packing and the 2^53 bubble guard use it), and f3's
+    scores stay exact against the oracle with such a menu"""
+    pb = gen.make_problem("12B")
+    f, b, a = strategy_menu(pb)
+    slow = (f.astype(np.int64) * 3).astype(np.uint32), (b.astype(np.int64) * 3).astype(np.uint32), a
+    m = dip.Model(pb, 0)
+    b0 = m.info["makespan_bound"]
+    m.set_strategies(slow, 10)
+    assert m.refresh_info()["makespan_bound"] > b0
+    cs = gen.generate(pb, 0, 64, p_mutate=0.0, p_bad=0.0)
+    check(pb, cs, menu=slow)
