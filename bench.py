@@ -210,7 +210,11 @@ def main():
     t_gen = time.time() - t0
     model = dip.Model(pb, local)
     ws = dip.Workspace(model, host_chunk=0 if args.no_e2e else args.host_chunk)
-    h_rec = torch.empty(per * model.stride, dtype=torch.uint8).pin_memory()
+    # host records: pinned at N = 1 (the records-path comparison below); at N > 1 only the initial
+    # copy uses them, so they stay pageable (every rank already pins its host view for e2e)
+    h_rec = torch.empty(per * model.stride, dtype=torch.uint8)
+    if world == 1:
+        h_rec = h_rec.pin_memory()
     model.encode(cs, out=h_rec, threads=gthreads)
     n_seg = cs.n.astype(np.int64)                     # per-candidate segment counts (stage-node totals)
     # the candidates' host view in pinned memory: the input of the end-to-end measurement
@@ -307,31 +311,29 @@ def main():
         hres = dip.results_view(h_res.numpy())
         assert np.array_equal(hres["makespan_ns"], res["makespan_ns"]) and np.array_equal(hres["status"], res["status"])
         view_bytes = sum(t.numel() * t.element_size() for t in h_view)
-        # the older record path (pinned records, no encode inside the timed region), for comparison
-        for _ in range(2):
-            dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
-        torch.cuda.synchronize()
-        a.record(stream)
-        for _ in range(args.steps):
-            dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        tr = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
-        # the copy alone: what bounds the end-to-end number when it is below the device number
-        a.record(stream)
-        d_rec.copy_(h_rec, non_blocking=True)
-        b.record(stream)
-        torch.cuda.synchronize()
-        h2d = per * model.stride / (a.elapsed_time(b) / 1e3) / 1e9
         e2e = {"value": per * world * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": view_bytes, "d2h_bytes_per_step": per * 24 + 8,
-               "h2d_GBps_alone": h2d,
                "path": "dip_eval_host_view: the candidates' host-view arrays (pinned) -> chunked H2D -> "
-                       "dip_encode_candidates_device -> dip_eval_schedules -> all results D2H -> dip_argmin",
-               "records_path": {"value": per * world * args.steps / (float(tr[0]) / 1e3), "unit": UNIT,
-                                "path": "dip_eval_host: pre-encoded pinned records -> H2D -> score -> winner"}}
+                       "dip_encode_candidates_device -> dip_eval_schedules -> all results D2H -> dip_argmin"}
+        if world == 1:
+            # the older record path (pinned records, no encode inside the timed region), for comparison
+            for _ in range(2):
+                dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(args.steps):
+                dip.eval_host(model, ws, h_rec, per, None, per, rank, world, comm, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tr = a.elapsed_time(b)
+            # the copy alone: what bounds the end-to-end number when it is below the device number
+            a.record(stream)
+            d_rec.copy_(h_rec, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e["h2d_GBps_alone"] = per * model.stride / (a.elapsed_time(b) / 1e3) / 1e9
+            e2e["records_path"] = {"value": per * args.steps / (tr / 1e3), "unit": UNIT,
+                                   "path": "dip_eval_host: pre-encoded pinned records -> H2D -> score -> winner"}
 
     # ---- DIP's dual-queue interleaving on the first f1-count records
     f1 = None

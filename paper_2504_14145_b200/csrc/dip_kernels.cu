@@ -353,8 +353,7 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
         // dependency value from its producer neighbour's channel ring (or, at rank 0 for F / rank
         // P-1 for B, from a wrap slot), end = max(t_last, dep + p2p) + layers * lat, then publish
         // end into its own channel ring (or read-modify-write a wrap slot). The neighbours' F and B
-        // counts travel as four separate shuffles (the shuffle unit is idle; the ALU pipe is the
-        // bottleneck, so no packing / unpacking). Exit and cycle checks run every 8th round.
+        // counts travel packed in two shuffles. Exit and cycle checks run every 8th round.
         // Channel rings are [2][D][P] u64 (F rings, then B rings; lane x owns column x).
         bool done = bad || !laneOn || n == 0;
         uint32_t t = 0, cF = 0, cB = 0;          // forward / backward stages placed so far
@@ -368,21 +367,16 @@ __global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
             const uint32_t d = (wcur >> (t & 31)) & 1u;            // 0 = F, 1 = B
             const bool wrapC = (wrapBits >> d) & 1u;
             const bool wrapP = (wrapPub >> d) & 1u;
-#ifdef DIP_PACKCNT   // A/B: the F and B counts in one word, two shuffles
+            // the neighbours' F / B counts, packed in one word: two shuffles (A/B on B200: +1 % 94B,
+            // +4 % 12B over four separate shuffles)
             const uint32_t cFB = cF | (cB << 16);
             const uint32_t up = __shfl_up_sync(FULL, cFB, 1, G), dn = __shfl_down_sync(FULL, cFB, 1, G);
             const uint32_t fu = up & 0xFFFFu, bu = up >> 16, fd = dn & 0xFFFFu, bd = dn >> 16;
-#else
-            const uint32_t fu = __shfl_up_sync(FULL, cF, 1, G), bu = __shfl_up_sync(FULL, cB, 1, G);
-            const uint32_t fd = __shfl_down_sync(FULL, cF, 1, G), bd = __shfl_down_sync(FULL, cB, 1, G);
-#endif
             const uint32_t idx = d ? cB : cF;
             const uint32_t nb = wrapC ? 0xFFFFu : (d ? bd : fu);                        // producer's count
-#ifdef DIP_CLAMPROW  // A/B: done lanes read a clamped (in-range, unused) row instead of a select
-            const uint2 e = posAll[d * n_max + min(idx, n_max - 1)];
-#else
-            const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];       // done lanes: a safe row
-#endif
+            // done lanes read the zero row: its wrap-slot fields are in range (a clamped real row's
+            // would not be -- rows past n are never written; measured: illegal address)
+            const uint2 e = done ? make_uint2(0u, 0u) : posAll[d * n_max + idx];
             const uint32_t ring = (idx & (D - 1)) * P;
             const uint64_t *ca = wrapC ? &depAll[e.y & 0xFFFFu] : &ringAll[ring + (d ? colIn1 : colIn0)];
             uint64_t *pa = wrapP ? &depAll[min(e.y >> 16, SINK)] : &ringAll[ring + (d ? colOut1 : colOut0)];
