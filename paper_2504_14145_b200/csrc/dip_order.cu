@@ -503,14 +503,15 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                         ainfo = 1u | (dir << 1) | ((uint32_t)(dir ? r - 1 : r + 1) << 2) | (s << 8);
                 }
                 __syncwarp();
-                if constexpr (G == 32) {
-                    // the placer's news: lanes to re-derive (wraps, itself) and the single ADD event,
-                    // which its target folds into its minima in O(1)
+                {
+                    // the placer's news (within the group): lanes to re-derive (wraps) and the single
+                    // ADD event, which its target folds into its minima in O(1)
                     const uint32_t who = (uint32_t)(gk & 31u);
                     const bool placed = gk != O_INF;
-                    const uint32_t msk = placed ? __shfl_sync(FULL, pl, (int)who) : 0u;
-                    const uint32_t ai = placed ? __shfl_sync(FULL, ainfo, (int)who) : 0u;
-                    const uint64_t av = placed ? __shfl_sync(FULL, addv, (int)who) : 0ull;
+                    const uint32_t msk0 = __shfl_sync(FULL, pl, (int)who, G);
+                    const uint32_t ai0 = __shfl_sync(FULL, ainfo, (int)who, G);
+                    const uint64_t av = __shfl_sync(FULL, addv, (int)who, G);
+                    const uint32_t msk = placed ? msk0 : 0u, ai = placed ? ai0 : 0u;
                     need = (((msk >> r) & 1u) ? 3u : 0u) | selfneed;
                     if ((ai & 1u) && ((ai >> 2) & 63u) == (uint32_t)r && !done) {
                         const uint32_t sa = ai >> 8;
@@ -521,8 +522,6 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                             if (cur + maxact <= bud || cur + actOf(sa) <= bud) tF = av < tF ? av : tF;
                         }
                     }
-                } else {
-                    need = 3u;
                 }
             }
         } else {

@@ -218,7 +218,7 @@ def test_strategy_menu_raises_the_makespan_bound():
     scores stay exact against the oracle with such a menu"""
     pb = gen.make_problem("12B")
     f, b, a = strategy_menu(pb)
-    slow = (f.astype(np.int64) * 3).astype(np.uint32), (b.astype(np.int64) * 3).astype(np.uint32), a
+    slow = (f.astype(np.int64) * 20).astype(np.uint32), (b.astype(np.int64) * 20).astype(np.uint32), a
     m = dip.Model(pb, 0)
     b0 = m.info["makespan_bound"]
     m.set_strategies(slow, 10)
