@@ -181,7 +181,7 @@ def main():
                     help="candidates for the f1 (dual-queue interleaving) measurement; 0 disables it")
     ap.add_argument("--f3-count", type=int, default=16384,
                     help="candidates for the f3 (per-layer memory optimisation) measurement; 0 disables it")
-    ap.add_argument("--f2-rounds", type=int, default=8, help="MCTS rounds for the f2 measurement; 0 disables it")
+    ap.add_argument("--f2-rounds", type=int, default=32, help="MCTS rounds for the f2 measurement; 0 disables it")
     ap.add_argument("--f2-leaves", type=int, default=256)
     ap.add_argument("--f2-rollouts", type=int, default=10)
     args = ap.parse_args()

@@ -15,9 +15,13 @@
  * per-rank forward/backward interleaving (reading R-1 of DESIGN.md).
  *
  * Beyond the scorer, the planner's other steps: dip_interleave (§5.2 dual-queue
- * interleaving), dip_search (§5.1 MCTS with batched GPU rollouts), dip_set_strategies /
- * dip_strategy_candidates / dip_memopt (§5.3 per-layer memory optimisation), dip_timeline /
- * dip_compile_plan / dip_validate_plan (§6.3 execution plans).
+ * interleaving; emits per-rank orders) and dip_eval_orders (schedules given as per-rank orders),
+ * dip_search (§5.1 MCTS with batched GPU rollouts, and the random / depth-first variants of the
+ * paper's comparison), dip_set_strategies / dip_strategy_candidates / dip_memopt /
+ * dip_set_memopt_solver / dip_memopt_stats (§5.3 per-layer memory optimisation, the per-rank ILP
+ * to a 5 % gap), dip_timeline / dip_compile_plan / dip_validate_plan (§6.3 execution plans).
+ * End to end: dip_encode_candidates_device and dip_eval_host_view (from the host view),
+ * dip_eval_host (from host records). dip_ubench_int measures the integer-pipe roofline peak.
  *
  * Units: time in integer nanoseconds (u64 accumulators), memory in KiB (u32).
  * All calls return dip_status (0 = DIP_OK); no C++ exception crosses the ABI.
