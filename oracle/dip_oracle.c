@@ -306,14 +306,16 @@ static void eval_one(const oproblem *pb, const ocands *cs, uint64_t x, ores *res
                 if (--indeg[d] == 0) queue[qt++] = d;
             }
         }
-        /* O9: memory per rank in slot order (order only; also for DEADLOCK) */
+        /* O9: memory per rank in slot order (order only; also for DEADLOCK), in u32 KiB (R-9: the
+         * load-time guard keeps a rank's activation sum below 2^32 KiB, so a valid order never wraps;
+         * an order that releases a backward before its forward -- a DEADLOCK -- wraps modulo 2^32) */
         uint32_t oom = 0;
         for (uint32_t r = 0; r < P; r++) {
-            uint64_t cur = 0, peak = 0;
+            uint32_t cur = 0, peak = 0;
             for (uint32_t t = 0; t < S; t++) {
                 uint32_t node = r * S + t;
-                if (dir[node] == 0) { cur += act[node]; if (cur > peak) peak = cur; }
-                else cur -= act[node];
+                if (dir[node] == 0) { cur += (uint32_t)act[node]; if (cur > peak) peak = cur; }
+                else cur -= (uint32_t)act[node];
             }
             if (peaks) peaks[r] = peak;
             if (peak > pb->budget_kib[r]) oom |= 1u << r;
