@@ -277,6 +277,9 @@ typedef struct {
                                  exploration (every rollout a uniformly random sequence from the root),
                                  2 = depth-first search (pre-order over the sequence tree, children
                                  in class order); rollouts / scoring / backpropagation unchanged */
+    double time_budget_ms;    /* > 0: stop after the first round that ends past this wall time
+                                 ("until a predefined time budget is exhausted"); the rounds
+                                 done are reported; 0 = run all `rounds` */
 } dip_search_params;
 
 typedef struct {

@@ -230,6 +230,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
     if (prm->policy < 0 || prm->policy > 2) { cudaFree(d_rec); cudaFree(d_res); cudaFree(d_ord); if (d_sel) cudaFree(d_sel);
         return fail(DIP_EINVAL, "policy must be 0 (MCTS), 1 (random) or 2 (DFS)"); }
     int dfs_cur = 0;
+    const double t_start = now();
     for (; rd < prm->rounds; rd++) {
         double t0 = now();
         // ---- selection + expansion of B leaves (virtual visits keep the batch diverse)
@@ -376,6 +377,7 @@ extern "C" dip_status dip_search(const dip_model *Md, dip_workspace *w, const ui
         }
         if (trace) trace[rd] = best;
         t_back += now() - t3;
+        if (prm->time_budget_ms > 0 && (now() - t_start) * 1e3 >= prm->time_budget_ms) { rd++; break; }
     }
     if (prof)
         std::fprintf(stderr, "dip_search: select %.1f ms, build %.1f ms, gpu %.1f ms, backprop %.1f ms over %u rounds\n",

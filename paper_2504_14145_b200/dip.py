@@ -53,7 +53,8 @@ class _CandBatch(ctypes.Structure):
 class _SearchParams(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("rounds", ctypes.c_uint32), ("leaves", ctypes.c_uint32),
                 ("rollouts", ctypes.c_uint32), ("threads", ctypes.c_int32), ("alpha", ctypes.c_double),
-                ("beta", ctypes.c_double), ("memopt", ctypes.c_int32), ("policy", ctypes.c_int32)]
+                ("beta", ctypes.c_double), ("memopt", ctypes.c_int32), ("policy", ctypes.c_int32),
+                ("time_budget_ms", ctypes.c_double)]
 
 
 class _SearchResult(ctypes.Structure):
@@ -374,14 +375,14 @@ def memopt_stats(ws: Workspace, stream=None) -> dict:
 
 def search(model: Model, ws: Workspace, split, seed: int, rounds: int, leaves: int, rollouts: int,
            alpha: float = 1.0, beta: float = 0.5, threads: int = 0, stream=None, memopt: bool = False,
-           policy: int = 0) -> dict:
+           policy: int = 0, time_budget_ms: float = 0.0) -> dict:
     """f2: MCTS over class orders for a fixed split with batched GPU rollouts (policy 1 /
     2: the random / depth-first exploration the paper compares against).
     Returns dict(found, makespan, score, trace, record (host bytes of the best rollout's split and
     priority orders), orders ([P, 2 n_max] its per-rank orders), ...)."""
     sp = np.ascontiguousarray(np.asarray(split, np.uint8).reshape(-1))
     prm = _SearchParams(seed & ((1 << 64) - 1), rounds, leaves, rollouts, threads, alpha, beta, 1 if memopt else 0,
-                        policy)
+                        policy, time_budget_ms)
     out = _SearchResult()
     rec = np.zeros(model.stride, np.uint8)
     ords = np.zeros((model.P, 2 * model.n_max), np.uint16)

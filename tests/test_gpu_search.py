@@ -82,3 +82,17 @@ def test_exploration_policies_match_oracle_trajectory(name, policy):
     o = oracle.search(pb, cs.split[0], seed=7, rounds=6, leaves=8, rollouts=4, policy=policy)
     assert np.array_equal(g["trace"], o["trace"]) and g["makespan"] == o["makespan"]
     assert np.array_equal(g["orders"], o["orders"]) and g["scored"] == o["scored"]
+
+
+def test_search_time_budget_stops_early_on_the_same_trajectory():
+    """the loop runs until a time budget is exhausted; the rounds it did are a prefix of
+    the full search's trajectory"""
+    pb = gen.make_problem("12B")
+    cs = gen.generate(pb, 0, 1, p_mutate=0, p_bad=0)
+    m = dip.Model(pb, 0)
+    ws = dip.Workspace(m)
+    full = dip.search(m, ws, cs.split[0], seed=3, rounds=40, leaves=64, rollouts=4, stream=torch.cuda.current_stream())
+    part = dip.search(m, ws, cs.split[0], seed=3, rounds=40, leaves=64, rollouts=4, time_budget_ms=1e-3,
+                      stream=torch.cuda.current_stream())
+    k = part["rounds_done"]
+    assert 1 <= k < 40 and np.array_equal(part["trace"][:k], full["trace"][:k])
