@@ -131,7 +131,7 @@ __device__ __noinline__ void spill_keep(unsigned long long *spill, uint32_t d, u
 // MODE 0: score the given schedules; MODE 2: score and record every stage's start / end (f4);
 // MODE 3: score with each stage pair's selected memory strategy (f3)
 template <int G, int MODE>
-__global__ void __launch_bounds__(256) dip_eval_kernel(const KParams kp) {
+__global__ void __launch_bounds__(768) dip_eval_kernel(const KParams kp) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t blob_bar;
     constexpr int CPG = 32 / G;
