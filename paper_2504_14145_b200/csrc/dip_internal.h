@@ -8,7 +8,10 @@
 
 namespace dipk {
 
-constexpr int RING_D = 4;              // depth of the smem inter-rank channels (exact spill beyond)
+#ifndef DIP_RING_D
+#define DIP_RING_D 2
+#endif
+constexpr int RING_D = DIP_RING_D;     // depth of the smem inter-rank channels (exact spill beyond; power of 2)
 constexpr uint64_t PEND_SHIFT = 56;    // wrap-dependency slot: pending count in bits 56..63
 constexpr uint64_t VAL_MASK = (1ull << PEND_SHIFT) - 1;
 
