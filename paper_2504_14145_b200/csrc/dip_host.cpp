@@ -271,10 +271,11 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
         kp.o_seq = oput(2 * 2 * M->n_pad);
         kp.o_posof = oput(2 * 2 * n_max);
         kp.o_sl = oput(2 * 8 * n_max);
-        kp.o_h = oput(2 * n_max);
         kp.o_bm = oput(2 * 4 * P * nwd);
         kp.o_sum = oput(2 * 4 * P);
         kp.o_mb = oput(3 * m * nm);
+        M->o_bytes_build = oo;          // the f1 build needs no ranks-done counters: they come last
+        kp.o_h = oput(2 * n_max);
         kp.o_bytes = oo;
     }
 
@@ -310,24 +311,29 @@ dip_status dip_load_cost_model(const dip_problem_desc *d, int cuda_device, dip_m
     M->smem = best_smem;
     M->grid = M->num_sms * best_bps;
     CUDA_TRY(dipk::prepare_eval(G, best_smem));
-    if (n_max <= 1024) {   // the per-rank-order kernel's shape (its ready-set summaries hold 32 words)
-        const size_t per_warp_o = (size_t)M->cpg * kp.o_bytes;
-        int bw = 0, bwpb = 0, bbps = 0;
-        size_t bsm = 0;
-        for (int wpb = 1; wpb <= 8; wpb++) {
-            const size_t sm = kp.blob_bytes + wpb * per_warp_o;
-            if (sm > smem_cap) break;
-            CUDA_TRY(dipk::prepare_order(G, sm));
-            int bps = 0;
-            CUDA_TRY(dipk::occupancy_order(G, wpb * 32, sm, &bps));
-            if (bps < 1) continue;
-            if (wpb * bps >= bw) { bw = wpb * bps; bwpb = wpb; bbps = bps; bsm = sm; }
+    if (n_max <= 1024) {   // the per-rank-order kernel's shapes (its ready-set summaries hold 32 words)
+        // (up to 24 warps per block, as the scorer; BUILD and TIME have their own per-schedule bytes)
+        size_t smax = 0;
+        for (int mode = 0; mode < 2; mode++) {
+            const size_t per_warp_o = (size_t)M->cpg * (mode ? M->o_bytes_build : kp.o_bytes);
+            int bw = 0, bwpb = 0, bbps = 0;
+            size_t bsm = 0;
+            for (int wpb = 1; wpb <= 24; wpb++) {
+                const size_t sm = kp.blob_bytes + wpb * per_warp_o;
+                if (sm > smem_cap) break;
+                CUDA_TRY(dipk::prepare_order(G, sm));
+                int bps = 0;
+                CUDA_TRY(dipk::occupancy_order(G, wpb * 32, sm, &bps));
+                if (bps < 1) continue;
+                if (wpb * bps >= bw) { bw = wpb * bps; bwpb = wpb; bbps = bps; bsm = sm; }
+            }
+            if (!bw) return fail(DIP_ERANGE, "per-schedule order working set does not fit in shared memory");
+            (mode ? M->ob_wpb : M->o_wpb) = bwpb;
+            (mode ? M->ob_smem : M->o_smem) = bsm;
+            (mode ? M->ob_grid : M->o_grid) = M->num_sms * bbps;
+            smax = std::max(smax, bsm);
         }
-        if (!bw) return fail(DIP_ERANGE, "per-schedule order working set does not fit in shared memory");
-        M->o_wpb = bwpb;
-        M->o_smem = bsm;
-        M->o_grid = M->num_sms * bbps;
-        CUDA_TRY(dipk::prepare_order(G, bsm));
+        CUDA_TRY(dipk::prepare_order(G, smax));
     }
 
     CUDA_TRY(cudaMalloc(&M->d_blob, kp.blob_bytes));
@@ -564,9 +570,12 @@ static dip_status launch_orders(const dip_model *M, dip_workspace *w, const void
         CUDA_TRY(cudaMemsetAsync(d_end, 0, count * M->P * 2ull * M->n_max * 8, s));
     }
     if (M->n_max > 1024) return fail(DIP_ERANGE, "per-rank-order kernel: n_max > 1024 (32 ready-set words)");
-    const int grid = (int)std::min<uint64_t>((uint64_t)M->o_grid,
-                                             std::max<uint64_t>(1, (count + M->cpg * M->o_wpb - 1) / (M->cpg * M->o_wpb)));
-    CUDA_TRY(dipk::launch_order(kp, M->G, om, grid, M->o_wpb * 32, M->o_smem, s));
+    const bool build = om == 1;
+    if (build) kp.o_bytes = M->o_bytes_build;
+    const int owpb = build ? M->ob_wpb : M->o_wpb, ogrid = build ? M->ob_grid : M->o_grid;
+    const int grid = (int)std::min<uint64_t>((uint64_t)ogrid,
+                                             std::max<uint64_t>(1, (count + M->cpg * owpb - 1) / (M->cpg * owpb)));
+    CUDA_TRY(dipk::launch_order(kp, M->G, om, grid, owpb * 32, build ? M->ob_smem : M->o_smem, s));
     g_launches++;
     return DIP_OK;
 }

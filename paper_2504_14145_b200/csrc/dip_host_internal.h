@@ -55,8 +55,11 @@ struct dip_model {
     dipk::KParams kp{};            // shape + blob + layout; per-launch fields filled per call
     int G = 32, cpg = 1, wpb = 1, bps = 1, grid = 1, num_sms = 148;
     size_t smem = 0;
-    int o_wpb = 1, o_grid = 1;         // per-rank-order kernel (dip_order.cu) shape
+    int o_wpb = 1, o_grid = 1;         // per-rank-order kernel (dip_order.cu) shape: TIME modes
     size_t o_smem = 0;
+    int ob_wpb = 1, ob_grid = 1;       // ... and the f1 BUILD mode (no ranks-done counters)
+    size_t ob_smem = 0;
+    uint32_t o_bytes_build = 0;
     uint64_t mk_bound = 0;
     // f3 (per-layer memory optimisation): strategy menu -> candidate table
     uint32_t n_strat = 0, S = 0;

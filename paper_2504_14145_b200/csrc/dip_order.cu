@@ -104,7 +104,7 @@ __device__ __forceinline__ bool wrap_publish(uint64_t *slot, uint64_t value) {
 // OM: 0 = TIME of explicit per-rank orders, 1 = BUILD (f1), 2 = TIME of a record's own orders (its
 // shared sequences + F/B bit rows: the record scorer on per-segment state)
 template <int G, int OM>
-__global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
+__global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
     constexpr bool BUILD = OM == 1;
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t blob_bar;
@@ -282,8 +282,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                 const uint32_t dc = segdec[s];
                 const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, j = (dc >> 11) & 15, k = (dc >> 15) & 0xFF;
                 const uint32_t Km1 = dc >> 23, q = b * nmod + i, M = Mb[q];
-                hF[s] = 0;
-                hB[s] = 0;
+                if (!BUILD) { hF[s] = 0; hB[s] = 0; }          // (BUILD's area has no counters)
                 if (j >= M) { slF[s] = 0; slB[s] = 0; rowx[s] = 0; continue; }
                 const uint32_t W = wtab[woff[q] + M * (M - 1) / 2 + j];
                 rowx[s] = (mi[i].tab_off + W) | ((mi[i].lay_off + k * P) << 12);
@@ -319,7 +318,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
         auto publish = [&](uint32_t d, uint32_t s, uint64_t end, uint64_t &addv) -> uint32_t {
             uint32_t full = 0;
             if (d == 0) {
-                hF[s] = (uint8_t)(r + 1);
+                if (!BUILD) hF[s] = (uint8_t)(r + 1);
                 if (!isLast) {
                     addv = end + tab[rowx[s] & 0xFFFu].w;
                     slF[s] = addv;
@@ -348,7 +347,7 @@ __global__ void __launch_bounds__(256) dip_order_kernel(const KParams kp) {
                     }
                 }
             } else {
-                hB[s] = (uint8_t)(P - r);
+                if (!BUILD) hB[s] = (uint8_t)(P - r);
                 if (!isFirst) {
                     addv = end + tab[rowx[s] & 0xFFFu].w;
                     slB[s] = addv;
