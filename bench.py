@@ -424,7 +424,9 @@ def main():
     f2 = None
     try:
         if args.f2_rounds > 0 and rank == 0:
-            dip.search(model, ws, cs.split[0], seed=pb.seed + 1, rounds=1, leaves=8, rollouts=2, stream=stream)  # warm-up
+            # warm-up at the same budget (the search's buffers and host tree sized as in the timed call)
+            dip.search(model, ws, cs.split[0], seed=pb.seed + 1, rounds=args.f2_rounds, leaves=args.f2_leaves,
+                       rollouts=args.f2_rollouts, stream=stream)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             sr = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,

@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
     uint16_t *eP = cbr + n_max;                                             // end of pair p's point range
     uint8_t *cn = reinterpret_cast<uint8_t *>(eP + n_max);                  // selected candidate | (count-1) << 4
     uint8_t *Mb = cn + n_max;                                               // [nq]
+    uint32_t *bmx = reinterpret_cast<uint32_t *>(                           // [n_max / 32] max of each
+        (reinterpret_cast<uintptr_t>(Mb + nq) + 3) & ~(uintptr_t)3);        //   32 keys (warm start)
 
     const int32_t INF = 0x7FFFFFFF;
     for (;;) {
@@ -428,22 +430,31 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                 dms[p] = dm;
             }
             __syncwarp();
+            // the max of every 32 keys, so that the argmax reads n / 32 words instead of n
+            const uint32_t nb = (n + 31) >> 5;
+            for (uint32_t b = 0; b < nb; b++) {
+                const uint32_t v = __reduce_max_sync(FULL, 32 * b + lane < n ? key[32 * b + lane] : 0u);
+                if (lane == 0) bmx[b] = v;
+            }
+            __syncwarp();
             for (;;) {
                 // the best pair not yet known to be blocked; its feasibility is checked only now
                 // (lazily): a pair whose step does not fit is blocked for good (the slack never grows)
-                uint32_t b0 = 0, b1 = 0;                   // two independent chains (ILP)
-                uint32_t p = lane;
-                for (; p + 32 < n; p += 64) { b0 = max(b0, key[p]); b1 = max(b1, key[p + 32]); }
-                if (p < n) b0 = max(b0, key[p]);
-                const uint32_t best = __reduce_max_sync(FULL, max(b0, b1));
+                uint32_t bm = 0;
+                for (uint32_t b = lane; b < nb; b += 32) bm = max(bm, bmx[b]);
+                const uint32_t best = __reduce_max_sync(FULL, bm);
                 if (best == 0) break;
                 const uint32_t a0 = 0xFFFFu - (best & 0xFFFFu), a1 = eP[a0], bdm = dms[a0];
                 int32_t mn = INF;
                 for (uint32_t k = a0 + lane; k < a1; k += 32) mn = min(mn, slack[k]);
                 mn = __reduce_min_sync(FULL, mn);
                 __syncwarp();
+                const uint32_t ab = a0 >> 5, ai = 32 * ab + lane;
                 if ((int64_t)bdm > (int64_t)mn) {          // blocked for good
                     if (lane == 0) key[a0] = 0;
+                    __syncwarp();
+                    const uint32_t v = __reduce_max_sync(FULL, ai < n ? key[ai] : 0u);
+                    if (lane == 0) bmx[ab] = v;
                     __syncwarp();
                     continue;
                 }
@@ -459,6 +470,9 @@ __global__ void __launch_bounds__(128) dip_memopt_kernel(const KParams kp, uint8
                     key[a0] = k;
                     dms[a0] = dm;
                 }
+                __syncwarp();
+                const uint32_t v = __reduce_max_sync(FULL, ai < n ? key[ai] : 0u);
+                if (lane == 0) bmx[ab] = v;
                 __syncwarp();
             }
         }

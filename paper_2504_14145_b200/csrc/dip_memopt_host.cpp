@@ -180,7 +180,7 @@ extern "C" dip_status dip_set_strategies(dip_model *M, uint32_t n_strat, const u
     M->kp.S = S;
     // selection kernel shape: 4 warps per block, per-warp working set in shared memory
     const uint32_t nmx = M->n_max, nq = M->m * nm;
-    M->mo_warp_bytes = up16(4 * ((nmx + 1) & ~1u) + nmx * (8 + 2 + 2 + 1) + nq);
+    M->mo_warp_bytes = up16(((4 * ((nmx + 1) & ~1u) + nmx * (8 + 2 + 2 + 1) + nq + 3) & ~3u) + 4 * ((nmx + 31) / 32));
     const size_t smem = 4 * (size_t)M->mo_warp_bytes;
     cudaDeviceProp prop;
     CUDA_TRY(cudaGetDeviceProperties(&prop, M->device));

@@ -105,13 +105,15 @@ def test_interleave_bad_and_non_linear_priorities():
     assert res["status"].tolist() == [oracle.ST_OK, oracle.ST_OK, oracle.ST_BAD]
 
 
-def test_interleave_tight_budgets():
-    # gating and gate lifting at scale (R-30, R-31): budgets at 60 % of the ungated peaks
+@pytest.mark.parametrize("name,count,frac", [("12B", 256, 0.6), ("toy", 512, 0.4), ("94B", 32, 0.7)])
+def test_interleave_tight_budgets(name, count, frac):
+    # gating and gate lifting at scale (R-30, R-31): budgets at a fraction of the ungated peaks
+    # (the kernel's several-ranks-per-step placement must still equal the serial greedy)
     import copy
-    pb = copy.deepcopy(gen.make_problem("12B"))
-    cs = gen.generate(pb, 0, 256, p_mutate=0.0, p_bad=0.0)
+    pb = copy.deepcopy(gen.make_problem(name))
+    cs = gen.generate(pb, 0, count, p_mutate=0.0, p_bad=0.0)
     base = oracle.interleave(pb, cs, threads=16)[1]
-    pb.budget_kib = (np.median(base.peaks, axis=0) * 0.6).astype(np.uint32)
+    pb.budget_kib = (np.median(base.peaks, axis=0) * frac).astype(np.uint32)
     res = check(pb, cs)
     assert (res["status"] == oracle.ST_OOM).any()
 
