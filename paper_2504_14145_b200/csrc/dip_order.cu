@@ -509,18 +509,16 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     else dir = bmin <= fmin ? 1u : 0u;
                     const uint64_t td = dir ? bmin : fmin, lim = td > tlast ? td : tlast;
                     const bool nogate = relax || cur + maxact <= bud;
-                    // the highest-priority (lowest position) stage starting as early as possible; the
-                    // same pass takes the minimum t_start of the rest of the queue (its new t_bw /
-                    // t_gated), so the placer rarely walks its ready set twice
+                    // the highest-priority (lowest position) stage starting as early as possible
                     uint32_t *mrow = (dir ? bmB : bmF) + r * nw;
                     uint32_t *msum = (dir ? smB : smF) + r;
                     const uint16_t *seq = dir ? seqB : seqF;
                     const uint64_t *sl = dir ? slB : slF;
                     uint32_t s = 0, pos = 0;
-                    uint64_t ts = 0, rest = O_INF;
+                    uint64_t ts = 0;
                     uint32_t ws = *msum;
                     bool found = false;
-                    while (ws) {
+                    while (ws && !found) {
                         const uint32_t w = __ffs(ws) - 1;
                         ws &= ws - 1;
                         uint32_t bits = mrow[w];
@@ -529,11 +527,10 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                             bits &= bits - 1;
                             const uint32_t sg = seq[p];
                             const uint64_t t = sl[sg] & VAL_MASK;
-                            if (!found && t <= lim && (dir || nogate || cur + actOf(sg) <= bud)) {
-                                s = sg; pos = p; ts = t; found = true;
-                            } else {
-                                rest = t < rest ? t : rest;
-                            }
+                            if (t > lim) continue;
+                            if (!dir && !nogate && cur + actOf(sg) > bud) continue;
+                            s = sg; pos = p; ts = t; found = true;
+                            break;
                         }
                     }
                     const uint32_t wrd = mrow[pos >> 5] & ~(1u << (pos & 31));
@@ -554,11 +551,11 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     last = (int)dir;
                     done = cnt == S2;
                     pl = publish(dir, s, end, addv);
-                    // the placer's own minima: its placed direction's queue minimum is `rest`; t_fw =
-                    // t_gated while no forward can be gated, else the forwards are re-derived
-                    if (dir) tB = rest; else tG = rest;
-                    if (cur + maxact <= bud) tF = tG;
-                    else selfneed = 1u;
+                    // the placer's own minima: its placed direction lost a stage; a backward placement
+                    // also lowered its memory, which can only un-gate forwards (none gated: t_fw = t_gated)
+                    if (dir == 0) selfneed = 1u;
+                    else if (cur + maxact <= bud) { selfneed = 2u; tF = tG; }
+                    else selfneed = 3u;
                     // an interior publication adds ONE ready stage to a neighbour (segment + 1)
                     if (dir == 0 && !isLast) aF = s + 1u;
                     if (dir == 1 && !isFirst) aB = s + 1u;

@@ -1,5 +1,7 @@
 """Lock-step round counts of the record scorer on generated candidates (CPU simulation): lane = rank
-(the kernel) vs two ranks per lane processed in alternating order within a round. Used for DESIGN.md §6.
+(the kernel) vs two ranks per lane processed in alternating order within a round, and vs a lane
+retiring up to R consecutive ready stages per round (rounds, and inner iterations = the sum over
+rounds of the most stages any lane retired: what a warp would execute). Used for DESIGN.md §6 / §9.
   PYTHONPATH=. python scripts/lockstep_rounds.py 94B 6"""
 import numpy as np, gen, sys
 sys.path.insert(0, '/root/repo')
@@ -66,6 +68,22 @@ def rounds_lockstep(P, ords, preds, n, pair=False):
         if rnd > 100000: return None
     return rnd
 
+def rounds_multi(P, ords, preds, R):
+    done = set(); cur = [0] * P; rnd = 0; iters = 0
+    total = sum(len(o) for o in ords); placed = 0
+    while placed < total:
+        rnd += 1; snap = set(done); mx = 0
+        for r in range(P):
+            k = 0
+            while k < R and cur[r] < len(ords[r]):
+                d, s = ords[r][cur[r]]
+                if not all((p in snap) or (p[2] == r and p in done) for p in preds(d, s, r)): break
+                done.add((d, s, r)); cur[r] += 1; placed += 1; k += 1
+            mx = max(mx, k)
+        iters += max(mx, 1)
+        if rnd > 100000: return None
+    return rnd, iters
+
 pb = gen.make_problem(sys.argv[1]); N = int(sys.argv[2])
 cs = gen.generate(pb, 0, N, p_mutate=0, p_bad=0)
 a = []; b = []
@@ -73,5 +91,6 @@ for x in range(N):
     ords, preds, n = orders_and_deps(pb, cs, x)
     r1 = rounds_lockstep(pb.P, ords, preds, n)
     r2 = rounds_lockstep(pb.P, ords, preds, n, pair=True)
-    if r1 and r2: a.append(r1); b.append(r2); print(x, 2 * n, r1, r2)
+    if r1 and r2: a.append(r1); b.append(r2); print(x, 2 * n, r1, r2, "multi (R: rounds, iterations)",
+                                                   {R: rounds_multi(pb.P, ords, preds, R) for R in (2, 4, 1000)})
 print("mean slots", np.mean([2 * int(cs.n[x]) for x in range(N)]), "lockstep", np.mean(a), "pair", np.mean(b))
