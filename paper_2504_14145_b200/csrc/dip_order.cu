@@ -422,21 +422,37 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
             const int nbl = r == 0 ? (int)P - 1 : r - 1, nbr = r + 1 >= (int)P ? 0 : r + 1;
             const uint32_t *mF = bmF + (laneOn ? r : 0) * nw, *mB = bmB + (laneOn ? r : 0) * nw;
             for (;;) {
-                if ((need & 1u) && !done) {        // re-derive the queue minima from the ready bitmaps
+                // re-derive the queue minima from the ready bitmaps (a ready stage's slot holds its
+                // t_start with a zero pending byte: no masking)
+                if ((need & 1u) && !done) {
                     tF = tG = O_INF;
-                    const bool nogate = cur + maxact <= bud;
                     uint32_t ws = smF[r];
-                    while (ws) {
-                        const uint32_t w = __ffs(ws) - 1;
-                        ws &= ws - 1;
-                        uint32_t bits = mF[w];
-                        while (bits) {
-                            const uint32_t p = 32 * w + __ffs(bits) - 1;
-                            bits &= bits - 1;
-                            const uint32_t s = seqF[p];
-                            const uint64_t t = slF[s] & VAL_MASK;
-                            tG = t < tG ? t : tG;
-                            if (nogate || cur + actOf(s) <= bud) tF = t < tF ? t : tF;
+                    if (cur + maxact <= bud) {     // no forward can be gated: t_fw = t_gated
+                        while (ws) {
+                            const uint32_t w = __ffs(ws) - 1;
+                            ws &= ws - 1;
+                            uint32_t bits = mF[w];
+                            while (bits) {
+                                const uint32_t p = 32 * w + __ffs(bits) - 1;
+                                bits &= bits - 1;
+                                const uint64_t t = slF[seqF[p]];
+                                tG = t < tG ? t : tG;
+                            }
+                        }
+                        tF = tG;
+                    } else {
+                        while (ws) {
+                            const uint32_t w = __ffs(ws) - 1;
+                            ws &= ws - 1;
+                            uint32_t bits = mF[w];
+                            while (bits) {
+                                const uint32_t p = 32 * w + __ffs(bits) - 1;
+                                bits &= bits - 1;
+                                const uint32_t s = seqF[p];
+                                const uint64_t t = slF[s];
+                                tG = t < tG ? t : tG;
+                                if (cur + actOf(s) <= bud) tF = t < tF ? t : tF;
+                            }
                         }
                     }
                 }
@@ -450,7 +466,7 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                         while (bits) {
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
-                            const uint64_t t = slB[seqB[p]] & VAL_MASK;
+                            const uint64_t t = slB[seqB[p]];
                             tB = t < tB ? t : tB;
                         }
                     }
@@ -526,7 +542,7 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
                             const uint32_t sg = seq[p];
-                            const uint64_t t = sl[sg] & VAL_MASK;
+                            const uint64_t t = sl[sg];
                             if (t > lim) continue;
                             if (!dir && !nogate && cur + actOf(sg) > bud) continue;
                             s = sg; pos = p; ts = t; found = true;
