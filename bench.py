@@ -428,14 +428,19 @@ def main():
             dip.search(model, ws, cs.split[0], seed=pb.seed + 1, rounds=args.f2_rounds, leaves=args.f2_leaves,
                        rollouts=args.f2_rollouts, stream=stream)
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            sr = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,
-                            rollouts=args.f2_rollouts, alpha=1.0, beta=0.5, stream=stream)
-            dt = time.perf_counter() - t0
+            # three identical searches (same seed, same result); the host tree and rollout encoding
+            # run on the shared host cores, so the rate is taken at the median wall time
+            walls = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                sr = dip.search(model, ws, cs.split[0], seed=pb.seed, rounds=args.f2_rounds, leaves=args.f2_leaves,
+                                rollouts=args.f2_rollouts, alpha=1.0, beta=0.5, stream=stream)
+                walls.append(time.perf_counter() - t0)
+            dt = float(np.median(walls))
             f2 = {"what": "dip_search: MCTS over class priorities (P:472-509), rollouts = priorities -> f1 interleaving "
                           "-> score, one batched GPU launch per round",
                   "rollouts_per_s": sr["scored"] / dt, "rollouts": sr["scored"], "rounds": sr["rounds_done"],
-                  "wall_s": dt, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
+                  "wall_s": dt, "wall_s_runs": walls, "best_makespan_ns": sr["makespan"], "best_score": sr["score"],
                   "trace_first_last": [float(sr["trace"][0]), float(sr["trace"][-1])], "tree_nodes": sr["tree_nodes"],
                   "same_split_template_fixed_order_ns": int(res["makespan_ns"][0]),
                   "same_split_template_f1_ns": int(f1_first["makespan_ns"]) if f1_first is not None else None}
