@@ -390,6 +390,10 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
             // ---------------- f1: the dual-queue greedy, one stage per step
             bool done = bad || !laneOn || n == 0;
             uint64_t tF = O_INF, tG = O_INF, tB = O_INF;   // min t_start: ungated F, any F, B
+            // the second smallest t_start of either queue (duplicates counted), valid while v2 has
+            // the direction's bit: removing a queue's minimum then needs no re-derivation
+            uint64_t tG2 = O_INF, tB2 = O_INF;
+            uint32_t v2 = 0;
             uint32_t need = 3;                             // bit 0: re-derive t_fw / t_gated, bit 1: t_bw
             int last = -1;
             uint32_t fstep = 0;
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                 // re-derive the queue minima from the ready bitmaps (a ready stage's slot holds its
                 // t_start with a zero pending byte: no masking)
                 if ((need & 1u) && !done) {
-                    tF = tG = O_INF;
+                    tF = tG = tG2 = O_INF;
                     uint32_t ws = smF[r];
                     if (cur + maxact <= bud) {     // no forward can be gated: t_fw = t_gated
                         while (ws) {
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                                 const uint32_t p = 32 * w + __ffs(bits) - 1;
                                 bits &= bits - 1;
                                 const uint64_t t = slF[seqF[p]];
+                                tG2 = t < tG2 ? (t < tG ? tG : t) : tG2;
                                 tG = t < tG ? t : tG;
                             }
                         }
@@ -450,14 +455,16 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                                 bits &= bits - 1;
                                 const uint32_t s = seqF[p];
                                 const uint64_t t = slF[s];
+                                tG2 = t < tG2 ? (t < tG ? tG : t) : tG2;
                                 tG = t < tG ? t : tG;
                                 if (cur + actOf(s) <= bud) tF = t < tF ? t : tF;
                             }
                         }
                     }
+                    v2 |= 1u;
                 }
                 if ((need & 2u) && !done) {
-                    tB = O_INF;
+                    tB = tB2 = O_INF;
                     uint32_t ws = smB[r];
                     while (ws) {
                         const uint32_t w = __ffs(ws) - 1;
@@ -467,9 +474,11 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
                             const uint64_t t = slB[seqB[p]];
+                            tB2 = t < tB2 ? (t < tB ? tB : t) : tB2;
                             tB = t < tB ? t : tB;
                         }
                     }
+                    v2 |= 2u;
                 }
                 const uint64_t tmin = done ? O_INF : (tF < tB ? tF : tB);
                 uint64_t gk = o_group_min<G>(tmin == O_INF ? O_INF : ((tmin << 5) | (uint64_t)r));
@@ -567,11 +576,25 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     last = (int)dir;
                     done = cnt == S2;
                     pl = publish(dir, s, end, addv);
-                    // the placer's own minima: its placed direction lost a stage; a backward placement
-                    // also lowered its memory, which can only un-gate forwards (none gated: t_fw = t_gated)
-                    if (dir == 0) selfneed = 1u;
-                    else if (cur + maxact <= bud) { selfneed = 2u; tF = tG; }
-                    else selfneed = 3u;
+                    // the placer's own minima: its placed direction lost the stage starting at ts --
+                    // the queue's minimum moves to the cached second smallest (then unknown), a stage
+                    // at the second smallest makes it unknown, a later one changes nothing; without a
+                    // known second the queue is re-derived. t_fw = t_gated while no forward can be
+                    // gated (a backward placement only lowers the memory), else the forwards are
+                    // re-derived.
+                    {
+                        uint64_t &m1 = dir ? tB : tG, &m2 = dir ? tB2 : tG2;
+                        const uint32_t bit = dir ? 2u : 1u;
+                        if (ts == m1) {
+                            if (v2 & bit) m1 = m2;
+                            else selfneed |= bit;
+                            v2 &= ~bit;
+                        } else if (ts == m2) {
+                            v2 &= ~bit;
+                        }
+                    }
+                    if (cur + maxact <= bud) tF = tG;
+                    else selfneed |= 1u;
                     // an interior publication adds ONE ready stage to a neighbour (segment + 1)
                     if (dir == 0 && !isLast) aF = s + 1u;
                     if (dir == 1 && !isFirst) aB = s + 1u;
@@ -591,10 +614,14 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     need = (wrapped ? 3u : 0u) | selfneed;
                     if (!done) {
                         if (r > 0 && sF && !(need & 1u)) {
-                            tG = vF < tG ? vF : tG;
+                            if (vF < tG) { tG2 = tG; tG = vF; v2 |= 1u; }   // the old minimum is second
+                            else if (vF < tG2) tG2 = vF;
                             if (cur + maxact <= bud || cur + actOf(sF - 1u) <= bud) tF = vF < tF ? vF : tF;
                         }
-                        if (r + 1 < (int)P && sB && !(need & 2u)) tB = vB < tB ? vB : tB;
+                        if (r + 1 < (int)P && sB && !(need & 2u)) {
+                            if (vB < tB) { tB2 = tB; tB = vB; v2 |= 2u; }
+                            else if (vB < tB2) tB2 = vB;
+                        }
                     }
                 }
             }
