@@ -319,41 +319,51 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
         // publication of stage (d, s) on rank r ending at `end`: on an interior rank the next rank's
         // ready time end + p2p goes into the segment's slot (BUILD: and the position into its ready
         // set); on the exit rank the wrap / join accumulators of the successor segments on the entry
-        // rank (which add their own p2p). Returns the lanes whose ready sets changed through a wrap
-        // (they re-derive their minima); an interior publication is the single-stage ADD event `add`.
+        // rank (which add their own p2p). BUILD bookkeeping: when exactly one stage became ready on
+        // the ring neighbour in d's direction (forward: r + 1, rank P-1 wraps to rank 0; backward:
+        // r - 1, rank 0 wraps to P-1), `aseg` = its segment + 1 and `addv` its ready time -- an ADD
+        // event the neighbour folds into its minima in O(1); the loss turnaround readies a backward
+        // stage on this rank itself (`selfB` = segment + 1); when several became ready the returned
+        // mask asks the entry rank to re-derive (bit 0: rank 0's forwards, bit 1: rank P-1's
+        // backwards).
         auto setbit = [&](uint32_t *bm, uint32_t *sm, uint32_t rr, uint32_t p) {
             bm[rr * nw + (p >> 5)] |= 1u << (p & 31);
             sm[rr] |= 1u << (p >> 5);
         };
-        auto publish = [&](uint32_t d, uint32_t s, uint64_t end, uint64_t &addv) -> uint32_t {
+        auto publish = [&](uint32_t d, uint32_t s, uint64_t end, uint64_t &addv, uint32_t &aseg,
+                           uint32_t &selfB) -> uint32_t {
             uint32_t full = 0;
             if (d == 0) {
                 if (!BUILD) hF[s] = (uint8_t)(r + 1);
                 if (!isLast) {
                     addv = end + tab[rowx[s] & 0xFFFu].w;
                     slF[s] = addv;
-                    if (BUILD) setbit(bmF, smF, r + 1, pofF[s]);
+                    if (BUILD) { setbit(bmF, smF, r + 1, pofF[s]); aseg = s + 1u; }
                 } else {
                     slF[s] = end;
                     const uint32_t dc = segdec[s];
                     const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, k = (dc >> 15) & 0xFF, K = (dc >> 23) + 1;
                     const uint32_t w = tab[rowx[s] & 0xFFFu].w;
                     if (k + 1 < K) {
-                        if (wrap_publish(&slF[s + 1], end + w) && BUILD) setbit(bmF, smF, 0, pofF[s + 1]);
-                        full |= 1u;
+                        if (wrap_publish(&slF[s + 1], end + w) && BUILD) {
+                            setbit(bmF, smF, 0, pofF[s + 1]);
+                            aseg = s + 2u;
+                            addv = slF[s + 1];
+                        }
                     } else if (Cc[b * nmod + i]) {
+                        uint32_t nr = 0, last = 0;
                         for (uint32_t c = 0; c < nmod; c++) {
                             if (!((mi[i].cons_mask >> c) & 1u)) continue;
                             const uint32_t Mc = Mb[b * nmod + c];
                             for (uint32_t jc = 0; jc < Mc; jc++) {
                                 const uint32_t t2 = sbase[b * nmod + c] + jc * mi[c].K;
-                                if (wrap_publish(&slF[t2], end + w) && BUILD) setbit(bmF, smF, 0, pofF[t2]);
+                                if (wrap_publish(&slF[t2], end + w) && BUILD) { setbit(bmF, smF, 0, pofF[t2]); nr++; last = t2; }
                             }
                         }
-                        full |= 1u;
+                        if (nr == 1) { aseg = last + 1u; addv = slF[last]; }
+                        else if (nr > 1) full |= 1u;
                     } else {                                   // loss turnaround (R-6)
-                        if (wrap_publish(&slB[s], end) && BUILD) setbit(bmB, smB, P - 1, pofB[s]);
-                        full |= 1u << (P - 1);
+                        if (wrap_publish(&slB[s], end) && BUILD) { setbit(bmB, smB, P - 1, pofB[s]); selfB = s + 1u; }
                     }
                 }
             } else {
@@ -361,26 +371,34 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                 if (!isFirst) {
                     addv = end + tab[rowx[s] & 0xFFFu].w;
                     slB[s] = addv;
-                    if (BUILD) setbit(bmB, smB, r - 1, pofB[s]);
+                    if (BUILD) { setbit(bmB, smB, r - 1, pofB[s]); aseg = s + 1u; }
                 } else {
                     slB[s] = end;
                     const uint32_t dc = segdec[s];
                     const uint32_t b = dc & 0xFF, i = (dc >> 8) & 7, k = (dc >> 15) & 0xFF;
                     if (k > 0) {                               // previous chunk, rank P-1 (+ its p2p)
-                        if (wrap_publish(&slB[s - 1], end + tab[rowx[s - 1] & 0xFFFu].w) && BUILD)
+                        if (wrap_publish(&slB[s - 1], end + tab[rowx[s - 1] & 0xFFFu].w) && BUILD) {
                             setbit(bmB, smB, P - 1, pofB[s - 1]);
+                            aseg = s;
+                            addv = slB[s - 1];
+                        }
                     } else {                                   // producers' last chunks (+ their p2p)
+                        uint32_t nr = 0, last = 0;
                         for (uint32_t pm = 0; pm < nmod; pm++) {
                             if (!((mi[i].prod_mask >> pm) & 1u)) continue;
                             const uint32_t Mp = Mb[b * nmod + pm];
                             for (uint32_t jp = 0; jp < Mp; jp++) {
                                 const uint32_t t2 = sbase[b * nmod + pm] + jp * mi[pm].K + mi[pm].K - 1;
-                                if (wrap_publish(&slB[t2], end + tab[rowx[t2] & 0xFFFu].w) && BUILD)
+                                if (wrap_publish(&slB[t2], end + tab[rowx[t2] & 0xFFFu].w) && BUILD) {
                                     setbit(bmB, smB, P - 1, pofB[t2]);
+                                    nr++;
+                                    last = t2;
+                                }
                             }
                         }
+                        if (nr == 1) { aseg = last + 1u; addv = slB[last]; }
+                        else if (nr > 1) full |= 2u;
                     }
-                    full |= 1u << (P - 1);
                 }
             }
             return full;
@@ -575,7 +593,8 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     cnt++;
                     last = (int)dir;
                     done = cnt == S2;
-                    pl = publish(dir, s, end, addv);
+                    uint32_t aseg = 0, selfB = 0;
+                    pl = publish(dir, s, end, addv, aseg, selfB);
                     // the placer's own minima: its placed direction lost the stage starting at ts --
                     // the queue's minimum moves to the cached second smallest (then unknown), a stage
                     // at the second smallest makes it unknown, a later one changes nothing; without a
@@ -595,9 +614,14 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     }
                     if (cur + maxact <= bud) tF = tG;
                     else selfneed |= 1u;
-                    // an interior publication adds ONE ready stage to a neighbour (segment + 1)
-                    if (dir == 0 && !isLast) aF = s + 1u;
-                    if (dir == 1 && !isFirst) aB = s + 1u;
+                    // ONE ready stage for the ring neighbour (segment + 1), and the turnaround's
+                    // backward stage on this rank itself
+                    if (dir == 0) aF = aseg; else aB = aseg;
+                    if (selfB) {
+                        const uint64_t v = slB[selfB - 1u];
+                        if (v < tB) { tB2 = tB; tB = v; v2 |= 2u; }
+                        else if (v < tB2) tB2 = v;
+                    }
                 }
                 __syncwarp();
                 {
@@ -605,20 +629,19 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     // P-1 only) and the ADD events from the left (forward) and right (backward)
                     // neighbours, which the target folds into its minima in O(1)
                     const uint32_t w0 = __ballot_sync(FULL, (pl & 1u) != 0) & gmask;
-                    const uint32_t wl = __ballot_sync(FULL, ((pl >> (P - 1)) & 1u) != 0) & gmask;
-                    const uint32_t sF = __shfl_up_sync(FULL, aF, 1, G);
-                    const uint64_t vF = __shfl_up_sync(FULL, addv, 1, G);
-                    const uint32_t sB = __shfl_down_sync(FULL, aB, 1, G);
-                    const uint64_t vB = __shfl_down_sync(FULL, addv, 1, G);
-                    const bool wrapped = (isFirst && w0) || (isLast && wl);
-                    need = (wrapped ? 3u : 0u) | selfneed;
+                    const uint32_t wl = __ballot_sync(FULL, (pl & 2u) != 0) & gmask;
+                    const uint32_t sF = __shfl_sync(FULL, aF, nbl, G);
+                    const uint64_t vF = __shfl_sync(FULL, addv, nbl, G);
+                    const uint32_t sB = __shfl_sync(FULL, aB, nbr, G);
+                    const uint64_t vB = __shfl_sync(FULL, addv, nbr, G);
+                    need = ((isFirst && w0) ? 1u : 0u) | ((isLast && wl) ? 2u : 0u) | selfneed;
                     if (!done) {
-                        if (r > 0 && sF && !(need & 1u)) {
+                        if (sF && !(need & 1u)) {
                             if (vF < tG) { tG2 = tG; tG = vF; v2 |= 1u; }   // the old minimum is second
                             else if (vF < tG2) tG2 = vF;
                             if (cur + maxact <= bud || cur + actOf(sF - 1u) <= bud) tF = vF < tF ? vF : tF;
                         }
-                        if (r + 1 < (int)P && sB && !(need & 2u)) {
+                        if (sB && !(need & 2u)) {
                             if (vB < tB) { tB2 = tB; tB = vB; v2 |= 2u; }
                             else if (vB < tB2) tB2 = vB;
                         }
@@ -686,7 +709,8 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                     cur = d ? cur - act : cur + act;
                     peak = cur > peak ? cur : peak;
                     uint64_t addv;
-                    publish(d, s, end, addv);
+                    uint32_t aseg, selfB;
+                    publish(d, s, end, addv, aseg, selfB);
                     if (d) bi++; else fi++;
                     cnt++;
                     if (OM == 2 && (cnt & 31) == 0) {      // next 32 F/B bits (the word after next prefetched)
