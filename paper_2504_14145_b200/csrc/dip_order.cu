@@ -454,12 +454,18 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                             const uint32_t w = __ffs(ws) - 1;
                             ws &= ws - 1;
                             uint32_t bits = mF[w];
-                            while (bits) {
+                            while (bits) {            // two stages per pass: independent load chains
                                 const uint32_t p = 32 * w + __ffs(bits) - 1;
                                 bits &= bits - 1;
-                                const uint64_t t = slF[seqF[p]];
+                                const uint32_t q = bits ? 32 * w + __ffs(bits) - 1 : p;
+                                bits &= bits - 1;
+                                const uint64_t t = slF[seqF[p]], u = slF[seqF[q]];
                                 tG2 = t < tG2 ? (t < tG ? tG : t) : tG2;
                                 tG = t < tG ? t : tG;
+                                if (q != p) {
+                                    tG2 = u < tG2 ? (u < tG ? tG : u) : tG2;
+                                    tG = u < tG ? u : tG;
+                                }
                             }
                         }
                         tF = tG;
@@ -488,12 +494,18 @@ __global__ void __launch_bounds__(768) dip_order_kernel(const KParams kp) {
                         const uint32_t w = __ffs(ws) - 1;
                         ws &= ws - 1;
                         uint32_t bits = mB[w];
-                        while (bits) {
+                        while (bits) {                // two stages per pass, as above
                             const uint32_t p = 32 * w + __ffs(bits) - 1;
                             bits &= bits - 1;
-                            const uint64_t t = slB[seqB[p]];
+                            const uint32_t q = bits ? 32 * w + __ffs(bits) - 1 : p;
+                            bits &= bits - 1;
+                            const uint64_t t = slB[seqB[p]], u = slB[seqB[q]];
                             tB2 = t < tB2 ? (t < tB ? tB : t) : tB2;
                             tB = t < tB ? t : tB;
+                            if (q != p) {
+                                tB2 = u < tB2 ? (u < tB ? tB : u) : tB2;
+                                tB = u < tB ? u : tB;
+                            }
                         }
                     }
                     v2 |= 2u;
